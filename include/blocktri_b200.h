@@ -1,0 +1,119 @@
+/*
+ * blocktri_b200.h -- C ABI of the B200-native block-tridiagonal SPD factor/solve engine.
+ *
+ * This is the drop-in boundary for the reference's hot path (arXiv 2509.03015, package
+ * `blocktri`).  The reference boundary is Python-level; each entry point below replaces one
+ * reference interface:
+ *
+ *   btd_plan_separators  <- plan_partition            /root/reference/pkg/src/blocktri/schur.py:75-95
+ *   btd_create           <- RecursionConfig + the level loop / _should_recurse
+ *                                                      schur.py:43-64, 289-326
+ *   btd_factorize        <- recursive_factorize        schur.py:289-318  (with _factorize_level 329-343,
+ *                           permute_split 98-138, factorize_btd_batch block_cholesky.py:60-68,
+ *                           _coupling_panels 141-153, compute_schur 156-193, serial_factorize
+ *                           block_cholesky.py:87-92)
+ *   btd_solve            <- recursive_solve            schur.py:346-374  (split_rhs 196-211,
+ *                           compute_separator_rhs 230-260, update_boundary 263-286,
+ *                           solve_btd_batch block_cholesky.py:71-84, assemble_solution 214-227,
+ *                           serial_solve block_cholesky.py:95-98)
+ *   btd_status           <- NotPositiveDefinite / LevelOverflow / DimensionMismatch
+ *                                                      errors.py:10-90
+ *
+ * Conventions (identical to the reference containers, core.py:23-71):
+ *   diag : N blocks of n x n, float64, row-major, contiguous           (N, n, n)
+ *   sub  : N-1 blocks, sub[i] = A_{i+1,i}                               (N-1, n, n)
+ *   rhs/x: N panels of n x d, row-major                                 (N, n, d)
+ * All data pointers are DEVICE pointers.  Every launch goes on the caller's CUDA stream
+ * (`stream` is a cudaStream_t; NULL = legacy default stream).  The input matrix and rhs are never
+ * written.  Device memory is caller-provided: query the sizes, allocate, pass the pointers.
+ */
+#ifndef BLOCKTRI_B200_H
+#define BLOCKTRI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define BTD_OK 0
+#define BTD_ERR_NOT_POSITIVE_DEFINITE 1 /* reference NotPositiveDefinite(pivot, level, member, block) */
+#define BTD_ERR_LEVEL_OVERFLOW 2        /* reference LevelOverflow */
+#define BTD_ERR_DIMENSION_MISMATCH 3    /* reference DimensionMismatch */
+#define BTD_ERR_INVALID_ARGUMENT 4      /* reference ValueError (config / plan preconditions) */
+#define BTD_ERR_UNSUPPORTED 5           /* block size outside the compiled kernel set */
+#define BTD_ERR_CUDA 6                  /* CUDA runtime error (message carries cudaGetErrorString) */
+#define BTD_ERR_NOT_FACTORED 7          /* reference ValueError("batch must be factorized ...") */
+
+/* RecursionConfig (schur.py:43-64). All knobs must be >= 1. */
+typedef struct btd_config {
+  int64_t crossover;      /* default 64 */
+  int64_t segment_length; /* rho, default 8 */
+  int64_t max_levels;     /* default 32 */
+  int32_t auto_crossover; /* default 0 */
+  int32_t reserved;
+} btd_config;
+
+/* Failure coordinates (errors.py:31-68). Coordinates that do not apply are -1. */
+typedef struct btd_status {
+  int32_t code;
+  int32_t pivot; /* 1-based pivot row inside the failing block */
+  int64_t level; /* recursion level (level-local coordinates, like the reference) */
+  int64_t member;
+  int64_t block;
+  char message[256];
+} btd_status;
+
+typedef struct btd_hierarchy btd_hierarchy; /* opaque: plan + device pointers of the factor */
+
+const char* btd_version(void);
+void btd_default_config(btd_config* cfg);
+
+/* One level of the partition plan, bit-exact with plan_partition (schur.py:75-95).
+ * separators_out may be NULL (count query). Requires num_blocks >= 3. */
+int btd_plan_separators(int64_t num_blocks, const btd_config* cfg, int64_t* separators_out,
+                        int64_t* count_out, btd_status* st);
+
+/* Plan the whole recursion for (N, n, cfg).  Fails with BTD_ERR_UNSUPPORTED when no kernel
+ * covers block size n. Host-only; no device work. */
+int btd_create(int64_t num_blocks, int64_t block_size, const btd_config* cfg, btd_hierarchy** out,
+               btd_status* st);
+void btd_destroy(btd_hierarchy* h);
+
+/* Recursion shape: levels that recurse, and the base (serial) block count.
+ * `overflow` = 1 when the plan would exceed max_levels (factorize then reports LevelOverflow). */
+int btd_num_levels(const btd_hierarchy* h, int64_t* num_levels, int64_t* base_blocks, int32_t* overflow);
+/* Level introspection: block count and separators of level `level` (separators_out may be NULL). */
+int btd_level_info(const btd_hierarchy* h, int64_t level, int64_t* num_blocks, int64_t* num_separators,
+                   int64_t* separators_out);
+
+/* Device memory: `persistent` holds the factor (kept for solves); `scratch` only lives during
+ * btd_factorize. Both 256-byte aligned. */
+int btd_factor_workspace(const btd_hierarchy* h, size_t* persistent_bytes, size_t* scratch_bytes);
+
+/* Factor. diag/sub: device pointers (read-only). With check != 0 the call synchronizes the stream
+ * once at the end and reports NotPositiveDefinite / LevelOverflow in `st`; with check == 0 it is
+ * fully asynchronous and btd_check() reports later. */
+int btd_factorize(btd_hierarchy* h, const double* diag, const double* sub, void* persistent, void* scratch,
+                  void* stream, int32_t check, btd_status* st);
+int btd_check(btd_hierarchy* h, void* stream, btd_status* st);
+
+/* Solve A X = B against a factored hierarchy. rhs (read-only) and x: device (N, n, d). The
+ * hierarchy is not modified, so concurrent solves on distinct buffers/streams are safe. */
+int btd_solve_workspace(const btd_hierarchy* h, int64_t num_columns, size_t* scratch_bytes);
+int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t num_columns, void* scratch,
+              void* stream, btd_status* st);
+
+/* Debug/introspection: copy level `level`'s factor blocks (Linv of every row and L_sub / coupling
+ * copies) into caller device buffers of N_l*n*n and (N_l-1)*n*n doubles.  level == num_levels
+ * addresses the base. */
+int btd_level_factor(const btd_hierarchy* h, int64_t level, double* linv_out, double* lsub_out,
+                     void* stream, btd_status* st);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BLOCKTRI_B200_H */

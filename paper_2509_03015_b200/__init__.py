@@ -1,0 +1,25 @@
+"""B200-native block-tridiagonal SPD factor/solve (recursive Schur complement, arXiv 2509.03015).
+
+Drop-in for the reference package's hot path (`blocktri.recursive_factorize` /
+`blocktri.recursive_solve` and the containers they use).  All arithmetic runs in hand-written
+sm_100a CUDA kernels behind the C ABI in include/blocktri_b200.h.
+"""
+
+from .core import (BlockRhs, BlockTridiagonalMatrix, FactorHierarchy, PartitionPlan, check_conformal,
+                   new_btd, new_rhs)
+from .errors import (AsymmetricBlock, BlockTriError, DeviceError, DimensionMismatch, InvalidDimensions,
+                     LevelOverflow, NotPositiveDefinite, SingularDiagonal)
+from .schur import (FactorLevel, RecursionConfig, level_factor, plan_partition, recursive_factorize,
+                    recursive_solve)
+from .synthgen import generate_spd_btd
+from .report import residual_report, btd_matmul
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AsymmetricBlock", "BlockRhs", "BlockTriError", "BlockTridiagonalMatrix", "DeviceError",
+    "DimensionMismatch", "FactorHierarchy", "FactorLevel", "InvalidDimensions", "LevelOverflow",
+    "NotPositiveDefinite", "PartitionPlan", "RecursionConfig", "SingularDiagonal", "btd_matmul",
+    "check_conformal", "generate_spd_btd", "level_factor", "new_btd", "new_rhs", "plan_partition",
+    "recursive_factorize", "recursive_solve", "residual_report",
+]

@@ -1,0 +1,570 @@
+// C-ABI implementation: recursion planning, workspace layout and kernel launches.
+// See include/blocktri_b200.h for the reference interface each entry point replaces.
+#include "../../include/blocktri_b200.h"
+
+#include <algorithm>
+#include <cstdarg>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "btd_factor.cuh"
+#include "btd_solve.cuh"
+
+namespace {
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+struct LevelPlan {
+  int64_t N = 0;  // blocks of this level's matrix
+  int64_t P = 0;  // separators (= blocks of the next level)
+  int64_t K = 0;  // segments
+  std::vector<int64_t> seps;
+  // persistent offsets
+  size_t off_seps = 0, off_linv = 0, off_lsub = 0;
+  // factor-scratch offsets: next level matrix + S_R scratch
+  size_t off_next_diag = 0, off_next_sub = 0, off_sr = 0;
+};
+
+}  // namespace
+
+struct btd_hierarchy {
+  int64_t N = 0, n = 0;
+  btd_config cfg{};
+  int nt = 0;
+  std::vector<LevelPlan> levels;
+  int64_t base_N = 0;
+  bool overflow = false;
+  size_t off_err = 0, off_base_linv = 0, off_base_lsub = 0;
+  size_t persistent_bytes = 0, scratch_bytes = 0;
+  char* persistent = nullptr;
+  bool factored = false;
+  bool pending_check = false;
+};
+
+namespace {
+
+void set_status(btd_status* st, int code, const char* fmt, ...) __attribute__((format(printf, 3, 4)));
+void set_status(btd_status* st, int code, const char* fmt, ...) {
+  if (!st) return;
+  st->code = code;
+  st->pivot = -1;
+  st->level = st->member = st->block = -1;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(st->message, sizeof(st->message), fmt, ap);
+  va_end(ap);
+}
+
+void clear_status(btd_status* st) {
+  if (!st) return;
+  st->code = BTD_OK;
+  st->pivot = -1;
+  st->level = st->member = st->block = -1;
+  st->message[0] = '\0';
+}
+
+int cuda_fail(btd_status* st, cudaError_t e, const char* where) {
+  set_status(st, BTD_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+  return BTD_ERR_CUDA;
+}
+
+bool config_ok(const btd_config* c) {
+  return c && c->crossover >= 1 && c->segment_length >= 1 && c->max_levels >= 1;
+}
+
+// plan_partition (bt/schur.py:75-95): separators at 0, rho+1, 2(rho+1), ...; the last block is always
+// a separator; a regular separator adjacent to it is dropped so the tail segment absorbs the gap.
+std::vector<int64_t> plan_separators(int64_t N, int64_t rho) {
+  std::vector<int64_t> s;
+  const int64_t step = rho + 1;
+  for (int64_t i = 0; i < N; i += step) s.push_back(i);
+  if (s.back() != N - 1) {
+    if (s.back() == N - 2) s.pop_back();
+    s.push_back(N - 1);
+  }
+  return s;
+}
+
+// _should_recurse (bt/schur.py:321-326)
+bool should_recurse(int64_t N, const btd_config& cfg) {
+  if (N < 3) return false;
+  if (cfg.auto_crossover) return plan_separators(N, cfg.segment_length).size() - 1 >= 2;
+  return N > cfg.crossover;
+}
+
+int pick_nt(int64_t n) {
+  if (n <= 8) return 8;
+  if (n <= 16) return 16;
+  if (n <= 32) return 32;
+  if (n <= 64) return 64;
+  return 0;
+}
+
+template <int NT>
+cudaError_t launch_factor(const btd::FactorArgs& a, unsigned grid, cudaStream_t s) {
+  using S = btd::FactorShape<NT>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(btd::factor_level_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)S::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  btd::factor_level_kernel<NT><<<grid, S::NTHREADS, S::SMEM, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t dispatch_factor(int nt, const btd::FactorArgs& a, unsigned grid, cudaStream_t s) {
+  switch (nt) {
+    case 8: return launch_factor<8>(a, grid, s);
+    case 16: return launch_factor<16>(a, grid, s);
+    case 32: return launch_factor<32>(a, grid, s);
+    case 64: return launch_factor<64>(a, grid, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int NT, int DC>
+cudaError_t launch_solve(const btd::SolveArgs& a, unsigned grid_x, cudaStream_t s) {
+  dim3 grid(grid_x, (unsigned)((a.d + DC - 1) / DC));
+  btd::solve_level_kernel<NT, DC><<<grid, btd::SolveShape<NT>::NTHREADS, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int NT>
+cudaError_t dispatch_solve_dc(const btd::SolveArgs& a, unsigned grid_x, cudaStream_t s) {
+  if (a.d == 1) return launch_solve<NT, 1>(a, grid_x, s);
+  if (a.d == 2) return launch_solve<NT, 2>(a, grid_x, s);
+  return launch_solve<NT, 4>(a, grid_x, s);
+}
+
+cudaError_t dispatch_solve(int nt, const btd::SolveArgs& a, unsigned grid_x, cudaStream_t s) {
+  switch (nt) {
+    case 8: return dispatch_solve_dc<8>(a, grid_x, s);
+    case 16: return dispatch_solve_dc<16>(a, grid_x, s);
+    case 32: return dispatch_solve_dc<32>(a, grid_x, s);
+    case 64: return dispatch_solve_dc<64>(a, grid_x, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+void decode_error(const btd::DevErr& e, btd_status* st) {
+  const long long j = (long long)(e.key >> 43);
+  const long long member = (long long)((e.key >> 16) & ((1ull << 27) - 1));
+  const int pivot = (int)(e.key & 0xffff);
+  set_status(st, BTD_ERR_NOT_POSITIVE_DEFINITE,
+             "matrix is not positive definite at pivot %d, block %lld, member %lld, level %d", pivot, j, member,
+             e.level);
+  st->pivot = pivot;
+  st->block = j;
+  st->member = member;
+  st->level = e.level;
+}
+
+int finish_check(btd_hierarchy* h, cudaStream_t stream, btd_status* st) {
+  btd::DevErr herr;
+  cudaError_t e = cudaMemcpyAsync(&herr, h->persistent + h->off_err, sizeof(herr), cudaMemcpyDeviceToHost, stream);
+  if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(copy error word)");
+  e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(sync)");
+  h->pending_check = false;
+  if (herr.key != btd::kNoErr) {
+    h->factored = false;
+    decode_error(herr, st);
+    return BTD_ERR_NOT_POSITIVE_DEFINITE;
+  }
+  if (h->overflow) {
+    h->factored = false;
+    set_status(st, BTD_ERR_LEVEL_OVERFLOW, "recursion needs more than max_levels=%lld levels",
+               (long long)h->cfg.max_levels);
+    return BTD_ERR_LEVEL_OVERFLOW;
+  }
+  h->factored = true;
+  return BTD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* btd_version(void) { return "blocktri_b200 0.1.0 (sm_100a)"; }
+
+void btd_default_config(btd_config* cfg) {
+  if (!cfg) return;
+  cfg->crossover = 64;
+  cfg->segment_length = 8;
+  cfg->max_levels = 32;
+  cfg->auto_crossover = 0;
+  cfg->reserved = 0;
+}
+
+int btd_plan_separators(int64_t num_blocks, const btd_config* cfg, int64_t* separators_out, int64_t* count_out,
+                        btd_status* st) {
+  clear_status(st);
+  if (!config_ok(cfg)) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "crossover, segment_length and max_levels must be >= 1");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  if (num_blocks < 3) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "cannot partition fewer than 3 block rows, got %lld",
+               (long long)num_blocks);
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  std::vector<int64_t> s = plan_separators(num_blocks, cfg->segment_length);
+  if (count_out) *count_out = (int64_t)s.size();
+  if (separators_out) std::copy(s.begin(), s.end(), separators_out);
+  return BTD_OK;
+}
+
+int btd_create(int64_t num_blocks, int64_t block_size, const btd_config* cfg, btd_hierarchy** out, btd_status* st) {
+  clear_status(st);
+  if (!out) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "out is NULL");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  *out = nullptr;
+  if (!config_ok(cfg)) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "crossover, segment_length and max_levels must be >= 1");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  if (num_blocks < 1 || block_size < 1) {
+    set_status(st, BTD_ERR_DIMENSION_MISMATCH, "need num_blocks >= 1 and block_size >= 1, got (%lld, %lld)",
+               (long long)num_blocks, (long long)block_size);
+    return BTD_ERR_DIMENSION_MISMATCH;
+  }
+  if (num_blocks >= (int64_t)INT_MAX) {
+    set_status(st, BTD_ERR_UNSUPPORTED, "num_blocks must be < 2^31");
+    return BTD_ERR_UNSUPPORTED;
+  }
+  const int nt = pick_nt(block_size);
+  if (!nt) {
+    set_status(st, BTD_ERR_UNSUPPORTED, "block size %lld has no sm_100a kernel in this build (n <= 64)",
+               (long long)block_size);
+    return BTD_ERR_UNSUPPORTED;
+  }
+  btd_hierarchy* h = new (std::nothrow) btd_hierarchy();
+  if (!h) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "out of host memory");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  h->N = num_blocks;
+  h->n = block_size;
+  h->cfg = *cfg;
+  h->nt = nt;
+  const size_t bb = (size_t)block_size * block_size * sizeof(double);
+
+  // ---- recursion plan (recursive_factorize level loop, bt/schur.py:298-318) ----
+  int64_t cur = num_blocks;
+  while (true) {
+    if (!should_recurse(cur, *cfg)) break;
+    if ((int64_t)h->levels.size() >= cfg->max_levels) {
+      h->overflow = true;
+      break;
+    }
+    LevelPlan lp;
+    lp.N = cur;
+    lp.seps = plan_separators(cur, cfg->segment_length);
+    lp.P = (int64_t)lp.seps.size();
+    lp.K = lp.P - 1;
+    int64_t maxlen = 0;
+    for (int64_t k = 0; k < lp.K; ++k) maxlen = std::max(maxlen, lp.seps[k + 1] - lp.seps[k] - 1);
+    if (maxlen > btd::kMaxBlockCoord) {
+      delete h;
+      set_status(st, BTD_ERR_UNSUPPORTED, "segment length %lld exceeds the device error-coordinate range",
+                 (long long)maxlen);
+      return BTD_ERR_UNSUPPORTED;
+    }
+    h->levels.push_back(std::move(lp));
+    cur = h->levels.back().P;
+  }
+  h->base_N = cur;
+
+  // ---- persistent layout: error word, per level seps/Linv/Lsub, base Linv/Lsub ----
+  size_t off = 0;
+  h->off_err = off;
+  off = align_up(off + sizeof(btd::DevErr));
+  for (auto& lp : h->levels) {
+    lp.off_seps = off;
+    off = align_up(off + (size_t)lp.P * sizeof(int));
+    lp.off_linv = off;
+    off = align_up(off + (size_t)lp.N * bb);
+    lp.off_lsub = off;
+    off = align_up(off + (size_t)(lp.N - 1) * bb);
+  }
+  if (!h->overflow) {
+    h->off_base_linv = off;
+    off = align_up(off + (size_t)h->base_N * bb);
+    h->off_base_lsub = off;
+    off = align_up(off + (size_t)std::max<int64_t>(h->base_N - 1, 1) * bb);
+  }
+  h->persistent_bytes = off;
+
+  // ---- factor scratch: per level, the next level's matrix and the S_R scratch ----
+  size_t so = 0;
+  for (auto& lp : h->levels) {
+    lp.off_next_diag = so;
+    so = align_up(so + (size_t)lp.P * bb);
+    lp.off_next_sub = so;
+    so = align_up(so + (size_t)(lp.P - 1) * bb);
+    lp.off_sr = so;
+    so = align_up(so + (size_t)lp.K * bb);
+  }
+  h->scratch_bytes = std::max<size_t>(so, kAlign);
+  *out = h;
+  return BTD_OK;
+}
+
+void btd_destroy(btd_hierarchy* h) { delete h; }
+
+int btd_num_levels(const btd_hierarchy* h, int64_t* num_levels, int64_t* base_blocks, int32_t* overflow) {
+  if (!h) return BTD_ERR_INVALID_ARGUMENT;
+  if (num_levels) *num_levels = (int64_t)h->levels.size();
+  if (base_blocks) *base_blocks = h->base_N;
+  if (overflow) *overflow = h->overflow ? 1 : 0;
+  return BTD_OK;
+}
+
+int btd_level_info(const btd_hierarchy* h, int64_t level, int64_t* num_blocks, int64_t* num_separators,
+                   int64_t* separators_out) {
+  if (!h || level < 0 || level >= (int64_t)h->levels.size()) return BTD_ERR_INVALID_ARGUMENT;
+  const LevelPlan& lp = h->levels[level];
+  if (num_blocks) *num_blocks = lp.N;
+  if (num_separators) *num_separators = lp.P;
+  if (separators_out) std::copy(lp.seps.begin(), lp.seps.end(), separators_out);
+  return BTD_OK;
+}
+
+int btd_factor_workspace(const btd_hierarchy* h, size_t* persistent_bytes, size_t* scratch_bytes) {
+  if (!h) return BTD_ERR_INVALID_ARGUMENT;
+  if (persistent_bytes) *persistent_bytes = h->persistent_bytes;
+  if (scratch_bytes) *scratch_bytes = h->scratch_bytes;
+  return BTD_OK;
+}
+
+int btd_factorize(btd_hierarchy* h, const double* diag, const double* sub, void* persistent, void* scratch,
+                  void* stream_, int32_t check, btd_status* st) {
+  clear_status(st);
+  if (!h || !diag || !persistent || !scratch || (h->N > 1 && !sub)) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_factorize: NULL argument");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  cudaStream_t stream = (cudaStream_t)stream_;
+  char* pers = (char*)persistent;
+  char* scr = (char*)scratch;
+  h->persistent = pers;
+  h->factored = false;
+  const int n = (int)h->n;
+  btd::DevErr* err = (btd::DevErr*)(pers + h->off_err);
+  btd::init_err_kernel<<<1, 1, 0, stream>>>(err);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(init)");
+
+  // separators of every level, generated on the device from the regular plan (no host sync):
+  // s_k = k (rho+1) for k < P-1 and s_{P-1} = N-1 (equivalent to plan_partition, bt/schur.py:75-95).
+  for (auto& lp : h->levels) {
+    const unsigned blocks = (unsigned)((lp.P + 255) / 256);
+    btd::fill_separators_kernel<<<blocks, 256, 0, stream>>>((int*)(pers + lp.off_seps), (int)lp.P, (int)lp.N,
+                                                            (int)(h->cfg.segment_length + 1));
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(seps)");
+
+  const double* cd = diag;
+  const double* cs = sub;
+  for (size_t l = 0; l < h->levels.size(); ++l) {
+    LevelPlan& lp = h->levels[l];
+    btd::FactorArgs a{};
+    a.diag = cd;
+    a.sub = cs;
+    a.seps = (const int*)(pers + lp.off_seps);
+    a.N = lp.N;
+    a.n = n;
+    a.K = (int)lp.K;
+    a.base = 0;
+    a.level = (int)l;
+    a.Linv = (double*)(pers + lp.off_linv);
+    a.Lsub = (double*)(pers + lp.off_lsub);
+    a.Sl = (double*)(scr + lp.off_next_diag);
+    a.Sr = (double*)(scr + lp.off_sr);
+    a.Ssub = (double*)(scr + lp.off_next_sub);
+    a.err = err;
+    e = dispatch_factor(h->nt, a, (unsigned)lp.K, stream);
+    if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(level kernel)");
+    btd::assemble_schur_diag_kernel<<<(unsigned)lp.P, 256, 0, stream>>>(cd, a.seps, a.Sl, a.Sr, (int)lp.K, n, err);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(assemble)");
+    cd = a.Sl;
+    cs = a.Ssub;
+  }
+  if (!h->overflow) {
+    btd::FactorArgs a{};
+    a.diag = cd;
+    a.sub = cs;
+    a.seps = nullptr;
+    a.N = h->base_N;
+    a.n = n;
+    a.K = 1;
+    a.base = 1;
+    a.level = (int)h->levels.size();
+    a.Linv = (double*)(pers + h->off_base_linv);
+    a.Lsub = (double*)(pers + h->off_base_lsub);
+    a.err = err;
+    e = dispatch_factor(h->nt, a, 1u, stream);
+    if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(base kernel)");
+  }
+  h->pending_check = true;
+  if (check) return finish_check(h, stream, st);
+  return BTD_OK;
+}
+
+int btd_check(btd_hierarchy* h, void* stream, btd_status* st) {
+  clear_status(st);
+  if (!h || !h->persistent) {
+    set_status(st, BTD_ERR_NOT_FACTORED, "hierarchy has not been factorized");
+    return BTD_ERR_NOT_FACTORED;
+  }
+  return finish_check(h, (cudaStream_t)stream, st);
+}
+
+int btd_solve_workspace(const btd_hierarchy* h, int64_t d, size_t* scratch_bytes) {
+  if (!h || d < 1) return BTD_ERR_INVALID_ARGUMENT;
+  const size_t pb = (size_t)h->n * d * sizeof(double);
+  size_t so = 0;
+  for (const auto& lp : h->levels) {
+    so = align_up(so + (size_t)lp.P * pb);  // next rhs
+    so = align_up(so + (size_t)lp.P * pb);  // next x
+    so = align_up(so + (size_t)lp.K * pb);  // f_R
+  }
+  if (scratch_bytes) *scratch_bytes = std::max<size_t>(so, kAlign);
+  return BTD_OK;
+}
+
+int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, void* scratch, void* stream_,
+              btd_status* st) {
+  clear_status(st);
+  if (!h || !rhs || !x || !scratch || d < 1) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_solve: NULL argument or d < 1");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  if (!h->factored && !h->pending_check) {
+    set_status(st, BTD_ERR_NOT_FACTORED, "hierarchy must be factorized before solving");
+    return BTD_ERR_NOT_FACTORED;
+  }
+  if (d > INT_MAX / 2) {
+    set_status(st, BTD_ERR_UNSUPPORTED, "too many rhs columns");
+    return BTD_ERR_UNSUPPORTED;
+  }
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const char* pers = h->persistent;
+  char* scr = (char*)scratch;
+  const btd::DevErr* err = (const btd::DevErr*)(pers + h->off_err);
+  const int n = (int)h->n;
+  const size_t pb = (size_t)h->n * d * sizeof(double);
+  const size_t L = h->levels.size();
+  std::vector<double*> rhs_l(L + 1), x_l(L + 1), fr_l(L);
+  rhs_l[0] = const_cast<double*>(rhs);
+  x_l[0] = x;
+  size_t so = 0;
+  for (size_t l = 0; l < L; ++l) {
+    const LevelPlan& lp = h->levels[l];
+    rhs_l[l + 1] = (double*)(scr + so);
+    so = align_up(so + (size_t)lp.P * pb);
+    x_l[l + 1] = (double*)(scr + so);
+    so = align_up(so + (size_t)lp.P * pb);
+    fr_l[l] = (double*)(scr + so);
+    so = align_up(so + (size_t)lp.K * pb);
+  }
+  cudaError_t e;
+  for (size_t l = 0; l < L; ++l) {
+    const LevelPlan& lp = h->levels[l];
+    btd::SolveArgs a{};
+    a.rhs = rhs_l[l];
+    a.Linv = (const double*)(pers + lp.off_linv);
+    a.Lsub = (const double*)(pers + lp.off_lsub);
+    a.seps = (const int*)(pers + lp.off_seps);
+    a.x = x_l[l];
+    a.fl = rhs_l[l + 1];
+    a.fr = fr_l[l];
+    a.N = lp.N;
+    a.n = n;
+    a.d = (int)d;
+    a.K = (int)lp.K;
+    a.mode = btd::kSolveDown;
+    a.err = err;
+    e = dispatch_solve(h->nt, a, (unsigned)lp.K, stream);
+    if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(down)");
+    btd::assemble_separator_rhs_kernel<<<(unsigned)lp.P, 128, 0, stream>>>(rhs_l[l], a.seps, rhs_l[l + 1], fr_l[l],
+                                                                            (int)lp.K, n, (int)d, err);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(assemble)");
+  }
+  {
+    btd::SolveArgs a{};
+    a.rhs = rhs_l[L];
+    a.Linv = (const double*)(pers + h->off_base_linv);
+    a.Lsub = (const double*)(pers + h->off_base_lsub);
+    a.x = x_l[L];
+    a.N = h->base_N;
+    a.n = n;
+    a.d = (int)d;
+    a.K = 1;
+    a.mode = btd::kSolveBase;
+    a.err = err;
+    e = dispatch_solve(h->nt, a, 1u, stream);
+    if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(base)");
+  }
+  for (size_t l = L; l-- > 0;) {
+    const LevelPlan& lp = h->levels[l];
+    btd::SolveArgs a{};
+    a.rhs = rhs_l[l];
+    a.Linv = (const double*)(pers + lp.off_linv);
+    a.Lsub = (const double*)(pers + lp.off_lsub);
+    a.seps = (const int*)(pers + lp.off_seps);
+    a.xsep = x_l[l + 1];
+    a.x = x_l[l];
+    a.N = lp.N;
+    a.n = n;
+    a.d = (int)d;
+    a.K = (int)lp.K;
+    a.mode = btd::kSolveUp;
+    a.err = err;
+    e = dispatch_solve(h->nt, a, (unsigned)lp.K, stream);
+    if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(up)");
+  }
+  return BTD_OK;
+}
+
+int btd_level_factor(const btd_hierarchy* h, int64_t level, double* linv_out, double* lsub_out, void* stream,
+                     btd_status* st) {
+  clear_status(st);
+  if (!h || !h->persistent || level < 0 || level > (int64_t)h->levels.size()) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_level_factor: bad level or unfactored hierarchy");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  const size_t bb = (size_t)h->n * h->n * sizeof(double);
+  size_t ol, os;
+  int64_t N;
+  if (level == (int64_t)h->levels.size()) {
+    ol = h->off_base_linv;
+    os = h->off_base_lsub;
+    N = h->base_N;
+  } else {
+    ol = h->levels[level].off_linv;
+    os = h->levels[level].off_lsub;
+    N = h->levels[level].N;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  if (linv_out) e = cudaMemcpyAsync(linv_out, h->persistent + ol, (size_t)N * bb, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess && lsub_out && N > 1)
+    e = cudaMemcpyAsync(lsub_out, h->persistent + os, (size_t)(N - 1) * bb, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(st, e, "btd_level_factor");
+  return BTD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// Device-side helpers shared by the block-tridiagonal factor/solve kernels (sm_100a).
+//
+// fp64 on B200: tcgen05 has no .kind::f64 (ptxas rejects it), so the fp64 tensor path is the
+// warp-synchronous `mma.sync.m8n8k4.f64` (SASS DMMA). Measured on this pool's B200:
+// DMMA 37.1 TFLOP/s, DFMA 34.1 TFLOP/s (profiles/fp64_peak_r01.json).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace btd {
+
+// ---------------------------------------------------------------------------------------------
+// Device error word.  The reference raises NotPositiveDefinite for the earliest block step j of
+// the failing level, lowest member at that step, with the 1-based pivot of that block
+// (bt/block_cholesky.py:24-42, bt/kernels.py:87-101,136-181).  We pack (j, member, pivot) so that
+// a single 64-bit atomicMin selects exactly that failure.
+// ---------------------------------------------------------------------------------------------
+struct DevErr {
+  unsigned long long key;  // (block << 43) | (member << 16) | pivot ; ~0ull == no error
+  int level;               // recursion level of the failure (INT_MAX == none)
+  int pad;
+};
+
+constexpr unsigned long long kNoErr = ~0ull;
+constexpr long long kMaxBlockCoord = (1ll << 20) - 1;
+constexpr long long kMaxMemberCoord = (1ll << 27) - 1;
+
+__device__ __forceinline__ void report_npd(DevErr* e, int level, long long block, long long member,
+                                           int pivot) {
+  unsigned long long j = (unsigned long long)(block < kMaxBlockCoord ? block : kMaxBlockCoord);
+  unsigned long long m = (unsigned long long)(member < kMaxMemberCoord ? member : kMaxMemberCoord);
+  unsigned long long key = (j << 43) | (m << 16) | (unsigned long long)(pivot & 0xffff);
+  atomicMin(&e->key, key);
+  atomicMin(&e->level, level);
+}
+
+__device__ __forceinline__ bool error_raised(const DevErr* e) {
+  return *((volatile const unsigned long long*)&e->key) != kNoErr;
+}
+
+// ---------------------------------------------------------------------------------------------
+// fp64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col).
+// Fragment ownership (lane l): a = A[l/4][l%4], b = B[l%4][l/4], d = {D[l/4][2(l%4)], D[l/4][2(l%4)+1]}.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------------------------------------
+// cp.async (LDGSTS) staging with zero fill.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Stage an n x n row-major global block into an NT x LD shared tile, zero-padding rows/cols >= n.
+template <int NT, int LD, int NTHREADS>
+__device__ __forceinline__ void stage_block_async(double* sm, const double* g, int n) {
+  if ((n & 1) == 0) {
+    constexpr int CPR = NT / 2;
+    for (int idx = threadIdx.x; idx < NT * CPR; idx += NTHREADS) {
+      const int r = idx / CPR, c = (idx % CPR) * 2;
+      const bool ok = (r < n) && (c < n);
+      cp_async16(sm + r * LD + c, ok ? (const void*)(g + (size_t)r * n + c) : (const void*)g, ok ? 16 : 0);
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < NT * NT; idx += NTHREADS) {
+      const int r = idx / NT, c = idx % NT;
+      const bool ok = (r < n) && (c < n);
+      cp_async8(sm + r * LD + c, ok ? (const void*)(g + (size_t)r * n + c) : (const void*)g, ok ? 8 : 0);
+    }
+  }
+}
+
+// Synchronous transposed staging: sm[r][c] = g[c][r] (zero padded).
+template <int NT, int LD, int NTHREADS>
+__device__ __forceinline__ void stage_block_transposed(double* sm, const double* g, int n) {
+  for (int idx = threadIdx.x; idx < NT * NT; idx += NTHREADS) {
+    const int c = idx / NT, r = idx % NT;  // read g row c (coalesced along r)
+    sm[r * LD + c] = (r < n && c < n) ? g[(size_t)c * n + r] : 0.0;
+  }
+}
+
+// Store the n x n leading part of a shared tile to a row-major global block.
+// lower_only: write zeros above the diagonal (triangular factors).
+template <int NT, int LD, int NTHREADS>
+__device__ __forceinline__ void store_block(double* g, const double* sm, int n, bool lower_only) {
+  if ((n & 1) == 0) {
+    const int cpr = n / 2;
+    for (int idx = threadIdx.x; idx < n * cpr; idx += NTHREADS) {
+      const int r = idx / cpr, c = (idx % cpr) * 2;
+      double2 v = *reinterpret_cast<const double2*>(sm + r * LD + c);
+      if (lower_only) {
+        if (c > r) v.x = 0.0;
+        if (c + 1 > r) v.y = 0.0;
+      }
+      *reinterpret_cast<double2*>(g + (size_t)r * n + c) = v;
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < n * n; idx += NTHREADS) {
+      const int r = idx / n, c = idx % n;
+      g[(size_t)r * n + c] = (lower_only && c > r) ? 0.0 : sm[r * LD + c];
+    }
+  }
+}
+
+// Plain global->global copy of an n x n block (used to keep the coupling blocks in the hierarchy).
+template <int NTHREADS>
+__device__ __forceinline__ void copy_block(double* dst, const double* src, int n) {
+  const int tot = n * n;
+  for (int i = threadIdx.x; i < tot; i += NTHREADS) dst[i] = src[i];
+}
+
+}  // namespace btd

@@ -1,0 +1,228 @@
+"""Recursive Schur-complement factor/solve on B200 (drop-in for `blocktri.schur`,
+/root/reference/pkg/src/blocktri/schur.py).
+
+``recursive_factorize`` / ``recursive_solve`` keep the reference signatures, argument meaning,
+ownership rules (input matrix and rhs never mutated; the hierarchy is immutable after the factor
+and safe for concurrent solves) and error behaviour (NotPositiveDefinite with level-local
+coordinates, LevelOverflow, DimensionMismatch).  All arithmetic runs in the sm_100a kernels of
+``libblocktri_b200.so`` behind the C ABI in include/blocktri_b200.h; this module only plans,
+allocates device memory through torch's caching allocator and maps status codes to exceptions.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .core import BlockRhs, BlockTridiagonalMatrix, FactorHierarchy, PartitionPlan, _is_torch
+from .errors import DeviceError, DimensionMismatch, LevelOverflow, NotPositiveDefinite
+
+
+@dataclass(frozen=True)
+class RecursionConfig:
+    """Tuning knobs of the recursive reduction (schur.py:43-64)."""
+
+    crossover: int = 64
+    segment_length: int = 8
+    max_levels: int = 32
+    auto_crossover: bool = False
+
+    def __post_init__(self):
+        if self.crossover < 1 or self.segment_length < 1 or self.max_levels < 1:
+            raise ValueError("crossover, segment_length and max_levels must be >= 1")
+
+    def _c(self) -> _native.BtdConfig:
+        return _native.BtdConfig(int(self.crossover), int(self.segment_length), int(self.max_levels),
+                                 1 if self.auto_crossover else 0, 0)
+
+
+@dataclass
+class FactorLevel:
+    """One recursion level: its partition (schur.py:67-72). The factor blocks stay on the device."""
+
+    plan: PartitionPlan
+    level: int
+
+
+@dataclass
+class BaseFactor:
+    """The serially factored base system (reference: FactorHierarchy.base, core.py:172)."""
+
+    num_blocks: int
+    block_size: int
+
+
+def _plan_from_separators(num_blocks: int, seps) -> PartitionPlan:
+    seps = tuple(int(s) for s in seps)
+    segments = tuple((a + 1, b) for a, b in zip(seps, seps[1:]))
+    return PartitionPlan(num_blocks, seps, segments)
+
+
+def plan_partition(num_blocks: int, config: RecursionConfig) -> PartitionPlan:
+    """Separators for one level (schur.py:75-95), computed by the native planner (bit-exact)."""
+    L = _native.lib()
+    st = _native.BtdStatus()
+    cnt = ctypes.c_int64()
+    cfg = config._c()
+    rc = L.btd_plan_separators(int(num_blocks), ctypes.byref(cfg), None, ctypes.byref(cnt), ctypes.byref(st))
+    if rc != _native.BTD_OK:
+        raise ValueError(st.message.decode())
+    out = (ctypes.c_int64 * cnt.value)()
+    L.btd_plan_separators(int(num_blocks), ctypes.byref(cfg), out, ctypes.byref(cnt), ctypes.byref(st))
+    plan = _plan_from_separators(num_blocks, out)
+    plan.validate()
+    return plan
+
+
+def _raise_status(st: _native.BtdStatus, rc: int):
+    msg = st.message.decode(errors="replace")
+    if rc == _native.BTD_ERR_NOT_POSITIVE_DEFINITE:
+        raise NotPositiveDefinite(int(st.pivot), level=int(st.level), member=int(st.member), block=int(st.block))
+    if rc == _native.BTD_ERR_LEVEL_OVERFLOW:
+        raise LevelOverflow(msg)
+    if rc == _native.BTD_ERR_DIMENSION_MISMATCH:
+        raise DimensionMismatch(msg)
+    if rc in (_native.BTD_ERR_INVALID_ARGUMENT, _native.BTD_ERR_NOT_FACTORED):
+        raise ValueError(msg)
+    if rc == _native.BTD_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise DeviceError(msg)
+
+
+class NativeFactor:
+    """Owns the C handle and the device memory of one factorization."""
+
+    def __init__(self, handle, persistent, device):
+        self.handle = handle
+        self.persistent = persistent
+        self.device = device
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                _native.lib().btd_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+def _device_matrix(matrix: BlockTridiagonalMatrix):
+    import torch
+    N, n = matrix.num_blocks, matrix.block_size
+    if _is_torch(matrix.diag):
+        dev = matrix.diag.device
+        if dev.type != "cuda":
+            diag = matrix.diag.to("cuda")
+            sub = matrix.sub.to("cuda")
+        else:
+            diag, sub = matrix.diag, matrix.sub
+        diag = diag.to(torch.float64).contiguous()
+        sub = sub.to(torch.float64).contiguous()
+    else:
+        diag = torch.from_numpy(np.ascontiguousarray(matrix.diag, dtype=np.float64)).to("cuda")
+        sub = torch.from_numpy(np.ascontiguousarray(matrix.sub, dtype=np.float64)).to("cuda")
+    if tuple(diag.shape) != (N, n, n) or tuple(sub.shape) != (max(N - 1, 0), n, n):
+        raise DimensionMismatch(f"matrix arenas {tuple(diag.shape)}, {tuple(sub.shape)} do not match (N={N}, n={n})")
+    return diag, sub
+
+
+def recursive_factorize(matrix: BlockTridiagonalMatrix, config: RecursionConfig | None = None,
+                        *, stream=None) -> FactorHierarchy:
+    """Factor an SPD block-tridiagonal system for repeated solves (schur.py:289-318).
+
+    Never mutates ``matrix``. Raises NotPositiveDefinite(pivot, level, member, block) with the
+    reference's level-local coordinates, LevelOverflow past ``max_levels``.
+    """
+    import torch
+    cfg = config or RecursionConfig()
+    L = _native.lib()
+    N, n = matrix.num_blocks, matrix.block_size
+    st = _native.BtdStatus()
+    handle = ctypes.c_void_p()
+    c = cfg._c()
+    rc = L.btd_create(N, n, ctypes.byref(c), ctypes.byref(handle), ctypes.byref(st))
+    if rc != _native.BTD_OK:
+        _raise_status(st, rc)
+    diag, sub = _device_matrix(matrix)
+    pers_b, scr_b = ctypes.c_size_t(), ctypes.c_size_t()
+    L.btd_factor_workspace(handle, ctypes.byref(pers_b), ctypes.byref(scr_b))
+    dev = diag.device
+    persistent = torch.empty(pers_b.value, dtype=torch.uint8, device=dev)
+    scratch = torch.empty(scr_b.value, dtype=torch.uint8, device=dev)
+    native = NativeFactor(handle, persistent, dev)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    rc = L.btd_factorize(handle, diag.data_ptr(), sub.data_ptr() if N > 1 else None, persistent.data_ptr(),
+                         scratch.data_ptr(), ctypes.c_void_p(s.cuda_stream), 1, ctypes.byref(st))
+    del scratch
+    if rc != _native.BTD_OK:
+        _raise_status(st, rc)
+    nl, nb, ov = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+    L.btd_num_levels(handle, ctypes.byref(nl), ctypes.byref(nb), ctypes.byref(ov))
+    levels = []
+    for lvl in range(nl.value):
+        lnb, lp = ctypes.c_int64(), ctypes.c_int64()
+        L.btd_level_info(handle, lvl, ctypes.byref(lnb), ctypes.byref(lp), None)
+        seps = (ctypes.c_int64 * lp.value)()
+        L.btd_level_info(handle, lvl, None, None, seps)
+        levels.append(FactorLevel(_plan_from_separators(lnb.value, seps), lvl))
+    return FactorHierarchy(N, n, levels, BaseFactor(nb.value, n), native)
+
+
+def recursive_solve(hierarchy: FactorHierarchy, rhs: BlockRhs, *, stream=None) -> BlockRhs:
+    """Solve against a stored factorization (schur.py:346-359).
+
+    Neither the hierarchy nor ``rhs`` is mutated.  numpy rhs -> numpy solution (host round
+    trip); torch CUDA rhs -> torch CUDA solution (device resident).
+    """
+    import torch
+    if rhs.num_blocks != hierarchy.num_blocks or rhs.block_size != hierarchy.block_size:
+        raise DimensionMismatch(
+            f"rhs ({rhs.num_blocks}, {rhs.block_size}) not conformal with "
+            f"hierarchy ({hierarchy.num_blocks}, {hierarchy.block_size})")
+    native = hierarchy._native
+    if native is None or not native.handle:
+        raise ValueError("hierarchy must be factorized before solving")
+    L = _native.lib()
+    host = not _is_torch(rhs.blocks)
+    if host:
+        b = torch.from_numpy(np.ascontiguousarray(rhs.blocks, dtype=np.float64)).to(native.device)
+    else:
+        b = rhs.blocks
+        if b.device != native.device:
+            b = b.to(native.device)
+        b = b.to(torch.float64).contiguous()
+    d = int(b.shape[2])
+    x = torch.empty_like(b)
+    scr_b = ctypes.c_size_t()
+    L.btd_solve_workspace(native.handle, d, ctypes.byref(scr_b))
+    scratch = torch.empty(scr_b.value, dtype=torch.uint8, device=native.device)
+    st = _native.BtdStatus()
+    s = stream if stream is not None else torch.cuda.current_stream(native.device)
+    rc = L.btd_solve(native.handle, b.data_ptr(), x.data_ptr(), d, scratch.data_ptr(),
+                     ctypes.c_void_p(s.cuda_stream), ctypes.byref(st))
+    if rc != _native.BTD_OK:
+        _raise_status(st, rc)
+    if host:
+        return BlockRhs(x.cpu().numpy())
+    return BlockRhs(x)
+
+
+def level_factor(hierarchy: FactorHierarchy, level: int):
+    """Debug view: (Linv, Lsub) device tensors of one level (level == len(levels) is the base)."""
+    import torch
+    native = hierarchy._native
+    L = _native.lib()
+    n = hierarchy.block_size
+    N = hierarchy.base.num_blocks if level == len(hierarchy.levels) else hierarchy.levels[level].plan.num_blocks
+    linv = torch.empty((N, n, n), dtype=torch.float64, device=native.device)
+    lsub = torch.empty((max(N - 1, 0), n, n), dtype=torch.float64, device=native.device)
+    st = _native.BtdStatus()
+    rc = L.btd_level_factor(native.handle, level, linv.data_ptr(), lsub.data_ptr() if N > 1 else None,
+                            ctypes.c_void_p(torch.cuda.current_stream(native.device).cuda_stream), ctypes.byref(st))
+    if rc != _native.BTD_OK:
+        _raise_status(st, rc)
+    return linv, lsub

@@ -1,0 +1,137 @@
+"""GPU parity: the sm_100a engine against the reference (golden fixtures from the real reference)
+and the CPU oracle, through the drop-in Python API -> C ABI -> CUDA kernels.
+
+Bars (BASELINE.json north_star): solution max|dX|/max|X| <= 1e-10, relative residual
+max_col ||AX-B||/||B|| <= 1e-12, bit-exact plans."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+import paper_2509_03015_b200 as pkg  # noqa: E402
+from oracle import blocktri_port as port  # noqa: E402
+
+REL_X = 1e-10
+REL_RES = 1e-12
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _cases(golden, prefix):
+    i = 0
+    while f"{prefix}{i}_meta" in golden:
+        yield i
+        i += 1
+
+
+def _solve(A, B, cfg):
+    h = pkg.recursive_factorize(A, cfg)
+    X = pkg.recursive_solve(h, B)
+    return h, X
+
+
+def test_golden_solutions(golden):
+    for i in _cases(golden, "solve"):
+        N, n, d, seed, cross, rho, auto = (int(v) for v in golden[f"solve{i}_meta"])
+        A, B = pkg.generate_spd_btd(N, n, d, seed)
+        cfg = pkg.RecursionConfig(crossover=cross, segment_length=rho, auto_crossover=bool(auto))
+        h, X = _solve(A, B, cfg)
+        ref = golden[f"solve{i}_x"]
+        rel = np.abs(X.blocks - ref).max() / max(np.abs(ref).max(), 1e-300)
+        assert rel <= REL_X, (i, (N, n, d), rel)
+        _, rres = pkg.residual_report(A, X, B)
+        assert rres <= REL_RES, (i, rres)
+        levels = [lvl.plan.num_blocks for lvl in h.levels] + [h.base.num_blocks]
+        assert levels == list(golden[f"solve{i}_levels"])
+        for li, lvl in enumerate(h.levels):
+            assert list(lvl.plan.separators) == list(golden[f"solve{i}_seps{li}"])
+
+
+def test_golden_npd_coordinates(golden):
+    for i in _cases(golden, "npd"):
+        N, n, seed, rho, cross = (int(v) for v in golden[f"npd{i}_meta"])
+        A, _ = pkg.generate_spd_btd(N, n, 1, seed)
+        for b in golden[f"npd{i}_bad"]:
+            A.diag[b] = -A.diag[b]
+        want = [int(v) for v in golden[f"npd{i}_coords"]]
+        with pytest.raises(pkg.NotPositiveDefinite) as e:
+            pkg.recursive_factorize(A, pkg.RecursionConfig(crossover=cross, segment_length=rho))
+        got = [e.value.pivot, e.value.level, e.value.member, e.value.block]
+        assert got == want, (i, got, want)
+
+
+SWEEP = [  # (N, n, d, crossover, rho)
+    (1, 1, 1, 64, 8), (1, 7, 2, 64, 8), (2, 5, 1, 64, 8), (3, 3, 3, 1, 1), (5, 2, 2, 2, 1),
+    (17, 1, 1, 2, 2), (33, 9, 2, 3, 3), (64, 16, 1, 64, 8), (65, 16, 1, 64, 8), (129, 17, 3, 8, 8),
+    (200, 31, 2, 16, 5), (300, 33, 1, 64, 8), (111, 47, 4, 9, 4), (250, 63, 1, 64, 8),
+    (260, 64, 3, 64, 8), (1000, 8, 1, 64, 8), (777, 12, 5, 10, 7), (90, 64, 6, 4, 2), (45, 6, 9, 3, 16),
+]
+
+
+@pytest.mark.parametrize("case", SWEEP, ids=[str(c) for c in SWEEP])
+def test_sweep_vs_oracle(case):
+    N, n, d, cross, rho = case
+    A, B = pkg.generate_spd_btd(N, n, d, seed=N * 7 + n)
+    cfg = pkg.RecursionConfig(crossover=cross, segment_length=rho)
+    _, X = _solve(A, B, cfg)
+    hh = port.factorize(A.diag, A.sub, cross, rho)
+    ref = port.solve(hh, B.blocks)
+    rel = np.abs(X.blocks - ref).max() / np.abs(ref).max()
+    assert rel <= REL_X, rel
+    _, rres = pkg.residual_report(A, X, B)
+    assert rres <= REL_RES, rres
+
+
+def test_device_tensors_roundtrip_and_no_mutation():
+    A, B = pkg.generate_spd_btd(500, 32, 3, seed=3)
+    dA = pkg.BlockTridiagonalMatrix(torch.from_numpy(A.diag).cuda(), torch.from_numpy(A.sub).cuda())
+    dB = pkg.BlockRhs(torch.from_numpy(B.blocks).cuda())
+    d0, s0, b0 = dA.diag.clone(), dA.sub.clone(), dB.blocks.clone()
+    h = pkg.recursive_factorize(dA)
+    X1 = pkg.recursive_solve(h, dB)
+    X2 = pkg.recursive_solve(h, dB)
+    assert torch.equal(dA.diag, d0) and torch.equal(dA.sub, s0) and torch.equal(dB.blocks, b0)
+    assert torch.equal(X1.blocks, X2.blocks)  # repeated solves independent (tests/test_schur.py:367-382)
+    _, rres = pkg.residual_report(dA, X1, dB)
+    assert rres <= REL_RES
+    Xh = pkg.recursive_solve(h, B)
+    assert np.array_equal(Xh.blocks, X1.blocks.cpu().numpy())
+
+
+def test_level_overflow_and_dimension_errors():
+    A, B = pkg.generate_spd_btd(300, 4, 1, seed=1)
+    with pytest.raises(pkg.LevelOverflow):
+        pkg.recursive_factorize(A, pkg.RecursionConfig(crossover=2, segment_length=1, max_levels=2))
+    h = pkg.recursive_factorize(A)
+    with pytest.raises(pkg.DimensionMismatch):
+        pkg.recursive_solve(h, pkg.BlockRhs(np.zeros((299, 4, 1))))
+
+
+def test_multi_column_equals_column_by_column():
+    A, B = pkg.generate_spd_btd(400, 24, 5, seed=9)
+    h = pkg.recursive_factorize(A)
+    X = pkg.recursive_solve(h, B).blocks
+    for c in range(5):
+        xc = pkg.recursive_solve(h, pkg.BlockRhs(np.ascontiguousarray(B.blocks[:, :, c:c + 1]))).blocks
+        assert np.abs(xc[:, :, 0] - X[:, :, c]).max() <= 1e-13 * np.abs(X).max()
+
+
+@pytest.mark.parametrize("cfg", [(1024, 32, 1), (65536, 64, 1), (1048576, 8, 1)],
+                         ids=["cfg1", "cfg2", "cfg3"])
+def test_baseline_configs_residual(cfg):
+    """Full BASELINE sizes: size-independent property (relative residual) + first rows vs oracle."""
+    N, n, d = cfg
+    A, B = pkg.generate_spd_btd(N, n, d, seed=0)
+    dA = pkg.BlockTridiagonalMatrix(torch.from_numpy(A.diag).cuda(), torch.from_numpy(A.sub).cuda())
+    dB = pkg.BlockRhs(torch.from_numpy(B.blocks).cuda())
+    h = pkg.recursive_factorize(dA)
+    X = pkg.recursive_solve(h, dB)
+    _, rres = pkg.residual_report(dA, X, dB)
+    assert rres <= REL_RES, rres
