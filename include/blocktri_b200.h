@@ -112,6 +112,12 @@ int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t num_
 int btd_level_factor(const btd_hierarchy* h, int64_t level, double* linv_out, double* lsub_out,
                      void* stream, btd_status* st);
 
+/* Optional per-launch timing: when enabled, btd_factorize records CUDA events on the caller's
+ * stream around every factor kernel (one per level, then the base).  btd_kernel_times returns the
+ * elapsed milliseconds of the last factorization's launches in that order. */
+int btd_profile_kernels(btd_hierarchy* h, int32_t enable);
+int btd_kernel_times(const btd_hierarchy* h, float* ms_out, int64_t cap, int64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

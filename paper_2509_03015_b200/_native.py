@@ -33,7 +33,7 @@ BTD_ERR_NOT_FACTORED = 7
 EXPORTED_SYMBOLS = (
     "btd_version", "btd_default_config", "btd_plan_separators", "btd_create", "btd_destroy",
     "btd_num_levels", "btd_level_info", "btd_factor_workspace", "btd_factorize", "btd_check",
-    "btd_solve_workspace", "btd_solve", "btd_level_factor",
+    "btd_solve_workspace", "btd_solve", "btd_level_factor", "btd_profile_kernels", "btd_kernel_times",
 )
 
 
@@ -96,6 +96,8 @@ def lib() -> ctypes.CDLL:
         L.btd_solve_workspace.argtypes = [c_vp, c_i64, P(c_sz)]
         L.btd_solve.argtypes = [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, P(BtdStatus)]
         L.btd_level_factor.argtypes = [c_vp, c_i64, c_vp, c_vp, c_vp, P(BtdStatus)]
+        L.btd_profile_kernels.argtypes = [c_vp, c_i32]
+        L.btd_kernel_times.argtypes = [c_vp, P(ctypes.c_float), c_i64, P(c_i64)]
         for name in EXPORTED_SYMBOLS:
             if name not in ("btd_version", "btd_default_config", "btd_destroy"):
                 getattr(L, name).restype = ctypes.c_int

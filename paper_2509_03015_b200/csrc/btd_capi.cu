@@ -44,9 +44,26 @@ struct btd_hierarchy {
   char* persistent = nullptr;
   bool factored = false;
   bool pending_check = false;
+  // optional per-launch timing of the factor kernels (btd_profile_kernels)
+  bool profile = false;
+  std::vector<cudaEvent_t> ev;
+  int nev = 0;
+  ~btd_hierarchy() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  }
 };
 
 namespace {
+
+void prof_mark(btd_hierarchy* h, cudaStream_t s) {
+  if (!h->profile) return;
+  if (h->nev >= (int)h->ev.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    h->ev.push_back(e);
+  }
+  cudaEventRecord(h->ev[h->nev++], s);
+}
 
 void set_status(btd_status* st, int code, const char* fmt, ...) __attribute__((format(printf, 3, 4)));
 void set_status(btd_status* st, int code, const char* fmt, ...) {
@@ -373,6 +390,7 @@ int btd_factorize(btd_hierarchy* h, const double* diag, const double* sub, void*
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(seps)");
+  h->nev = 0;
 
   const double* cd = diag;
   const double* cs = sub;
@@ -393,7 +411,9 @@ int btd_factorize(btd_hierarchy* h, const double* diag, const double* sub, void*
     a.Sr = (double*)(scr + lp.off_sr);
     a.Ssub = (double*)(scr + lp.off_next_sub);
     a.err = err;
+    prof_mark(h, stream);
     e = dispatch_factor(h->nt, a, (unsigned)lp.K, stream);
+    prof_mark(h, stream);
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(level kernel)");
     btd::assemble_schur_diag_kernel<<<(unsigned)lp.P, 256, 0, stream>>>(cd, a.seps, a.Sl, a.Sr, (int)lp.K, n, err);
     e = cudaGetLastError();
@@ -414,7 +434,9 @@ int btd_factorize(btd_hierarchy* h, const double* diag, const double* sub, void*
     a.Linv = (double*)(pers + h->off_base_linv);
     a.Lsub = (double*)(pers + h->off_base_lsub);
     a.err = err;
+    prof_mark(h, stream);
     e = dispatch_factor(h->nt, a, 1u, stream);
+    prof_mark(h, stream);
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(base kernel)");
   }
   h->pending_check = true;
@@ -564,6 +586,36 @@ int btd_level_factor(const btd_hierarchy* h, int64_t level, double* linv_out, do
   if (e == cudaSuccess && lsub_out && N > 1)
     e = cudaMemcpyAsync(lsub_out, h->persistent + os, (size_t)(N - 1) * bb, cudaMemcpyDeviceToDevice, s);
   if (e != cudaSuccess) return cuda_fail(st, e, "btd_level_factor");
+  return BTD_OK;
+}
+
+#ifdef BTD_PHASE_PROF
+int btd_debug_phase_cycles(unsigned long long* out16, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out16, btd::g_phase_cycles, 16 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(btd::g_phase_cycles, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
+
+int btd_profile_kernels(btd_hierarchy* h, int32_t enable) {
+  if (!h) return BTD_ERR_INVALID_ARGUMENT;
+  h->profile = enable != 0;
+  return BTD_OK;
+}
+
+int btd_kernel_times(const btd_hierarchy* h, float* ms_out, int64_t cap, int64_t* count) {
+  if (!h) return BTD_ERR_INVALID_ARGUMENT;
+  const int64_t n = h->nev / 2;
+  if (count) *count = n;
+  for (int64_t i = 0; i < n && i < cap && ms_out; ++i) {
+    cudaError_t e = cudaEventSynchronize(h->ev[2 * i + 1]);
+    if (e != cudaSuccess) return BTD_ERR_CUDA;
+    cudaEventElapsedTime(&ms_out[i], h->ev[2 * i], h->ev[2 * i + 1]);
+  }
   return BTD_OK;
 }
 

@@ -95,7 +95,18 @@ __device__ __forceinline__ void stage_block_transposed(double* sm, const double*
 // lower_only: write zeros above the diagonal (triangular factors).
 template <int NT, int LD, int NTHREADS>
 __device__ __forceinline__ void store_block(double* g, const double* sm, int n, bool lower_only) {
-  if ((n & 1) == 0) {
+  if (n == NT) {
+    constexpr int CPR = NT / 2;
+    for (int idx = threadIdx.x; idx < NT * CPR; idx += NTHREADS) {
+      const int r = idx / CPR, c = (idx % CPR) * 2;
+      double2 v = *reinterpret_cast<const double2*>(sm + r * LD + c);
+      if (lower_only) {
+        if (c > r) v.x = 0.0;
+        if (c + 1 > r) v.y = 0.0;
+      }
+      *reinterpret_cast<double2*>(g + (size_t)r * NT + c) = v;
+    }
+  } else if ((n & 1) == 0) {
     const int cpr = n / 2;
     for (int idx = threadIdx.x; idx < n * cpr; idx += NTHREADS) {
       const int r = idx / cpr, c = (idx % cpr) * 2;

@@ -25,6 +25,22 @@
 
 namespace btd {
 
+#ifdef BTD_PHASE_PROF
+__device__ unsigned long long g_phase_cycles[16];
+#define BTD_PHASE_INIT() long long _ph_last = clock64();
+#define BTD_PHASE(i)                                                        \
+  do {                                                                      \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                              \
+      long long _now = clock64();                                           \
+      atomicAdd(&g_phase_cycles[i], (unsigned long long)(_now - _ph_last)); \
+      _ph_last = _now;                                                      \
+    }                                                                       \
+  } while (0)
+#else
+#define BTD_PHASE_INIT()
+#define BTD_PHASE(i)
+#endif
+
 struct FactorArgs {
   const double* diag;  // level matrix: (N, n, n)
   const double* sub;   // (N-1, n, n), sub[i] = A_{i+1,i}
@@ -58,7 +74,9 @@ struct FactorShape {
   static constexpr int MAXG = (NG + NW - 1) / NW;
   static constexpr int MAXD = (ND + NW - 1) / NW;
   static constexpr size_t SMEM = (size_t)3 * NT * LD * sizeof(double);
+  static constexpr int MINB = NT == 64 ? 2 : NT == 32 ? 4 : 8;  // CTAs per SM to overlap pivot latency
   static_assert(NT / 8 == NW, "one trtri leaf per warp");
+  static_assert(NTHREADS == 4 * NT, "potrf thread map: 8 panel columns x NT/2 row pairs");
 };
 
 __device__ __forceinline__ void tri_decode(int s, int& r, int& c) {
@@ -67,144 +85,222 @@ __device__ __forceinline__ void tri_decode(int s, int& r, int& c) {
   c = s - r * (r + 1) / 2;
 }
 
+// Inverse of one 8x8 lower-triangular diagonal tile, in place (lanes 0..7: one column each).
+// 1/L_ii was stored at DL[i][NT] by the panel factorization.
+template <int NT>
+__device__ __forceinline__ void leaf_inverse(double* DL, int d0, int lane) {
+  constexpr int LD = FactorShape<NT>::LD;
+  double x[8];
+  if (lane < 8) {
+    const int c = lane;
+    double ri[8], row[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ri[i] = DL[(d0 + i) * LD + NT];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = (i == c) ? ri[i] : 0.0;
+#pragma unroll
+    for (int i = 1; i < 8; ++i) {
+#pragma unroll
+      for (int mm = 0; mm < i; ++mm) row[mm] = DL[(d0 + i) * LD + d0 + mm];
+      double s0 = 0.0, s1 = 0.0;  // x[mm] == 0 for mm < c, so no predicate is needed
+#pragma unroll
+      for (int mm = 0; mm < i; ++mm) {
+        if (mm & 1)
+          s1 = fma(row[mm], x[mm], s1);
+        else
+          s0 = fma(row[mm], x[mm], s0);
+      }
+      if (i > c) x[i] = -(s0 + s1) * ri[i];
+    }
+  }
+  __syncwarp();
+  if (lane < 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) DL[(d0 + i) * LD + d0 + lane] = x[i];
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // In-place Cholesky + triangular inverse of the NT x NT tile DL (lower triangle is read).
-// Panel-blocked (8 columns): unblocked elimination inside the panel, DMMA trailing update.
 // Returns the 1-based first non-positive pivot (reference _first_bad_pivot, bt/kernels.py:136-152;
-// failure test is `pivot <= 0` like the LAPACK/OpenBLAS path, so NaN propagates silently),
-// or 0. The result is uniform across the CTA.
+// failure test is `pivot <= 0` like the LAPACK/OpenBLAS path, so NaN propagates silently, SURVEY
+// §5), or 0.  The result is uniform across the CTA.
+//
+// Panel-blocked right-looking Cholesky.  Each 8-column panel is factored by ONE warp in
+// registers (lane l owns panel rows p0+l and p0+l+32): the pivot chain is latency bound
+// (shfl -> rsqrt -> fma per column), so it is kept short in instructions and leaves the issue
+// slots to the co-resident CTA.  While warp 0 factors panel p, another warp inverts the
+// 8x8 diagonal tile of panel p-1 (trtri leaf).  The trailing update of the lower 8x8 tiles is a
+// batched DMMA rank-8 update by all warps; the inverse is finished by recursive doubling on DMMA.
 // ------------------------------------------------------------------------------------------
 template <int NT>
 __device__ int potrf_trtri(double* DL) {
   using S = FactorShape<NT>;
   constexpr int LD = S::LD;
-  constexpr int NTHREADS = S::NTHREADS;
   constexpr int NW = S::NW;
+  constexpr int NP = NT / 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ int s_fail;
+  BTD_PHASE_INIT();
+  __syncthreads();
 
-  for (int p = 0; p < NT / 8; ++p) {
+  for (int p = 0; p < NP; ++p) {
     const int p0 = p * 8;
-    double sprev = 1.0;
-    for (int kk = 0; kk < 8; ++kk) {
-      const int k = p0 + kk;
-      __syncthreads();
-      const double d = DL[k * LD + k];
-      // deferred scaling of the previous panel column (nobody reads it in this phase)
-      if (kk > 0) {
-        const double rs = 1.0 / sprev;
-        for (int i = k - 1 + tid; i < NT; i += NTHREADS)
-          DL[i * LD + k - 1] = (i == k - 1) ? sprev : DL[i * LD + k - 1] * rs;
+    if (warp == 0) {
+      const int ra = p0 + lane, rb = p0 + lane + 32;
+      const bool ha = ra < NT, hb = rb < NT;
+      double va[8], vb[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        va[c] = ha ? DL[ra * LD + p0 + c] : 0.0;
+        vb[c] = hb ? DL[rb * LD + p0 + c] : 0.0;
       }
-      if (d <= 0.0) return k + 1;
-      const double dinv = 1.0 / d;
-      // update the panel columns c in (k, p0+8), rows i >= c
-      const int ncols = p0 + 7 - k;  // columns k+1 .. p0+7
-      if (ncols > 0) {
-        const int nrows = NT - k - 1;  // rows k+1 .. NT-1
-        for (int e = tid; e < nrows * ncols; e += NTHREADS) {
-          const int i = k + 1 + e / ncols;
-          const int c = k + 1 + e % ncols;
-          if (c <= i) DL[i * LD + c] -= DL[i * LD + k] * DL[c * LD + k] * dinv;
+      // Branch-free pivot chain: a data-dependent `break` here costs ~40% of the chain latency
+      // (measured, tools/panel_bench.cu); a failed pivot only poisons values that are discarded.
+      int fail = 0;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const double d = __shfl_sync(0xffffffffu, va[kk], kk);
+        double lck[8];
+#pragma unroll
+        for (int c = kk + 1; c < 8; ++c) lck[c] = __shfl_sync(0xffffffffu, va[kk], c);
+        fail = (fail == 0 && d <= 0.0) ? p0 + kk + 1 : fail;
+        const double rinv = rsqrt(d);
+        const double dinv = rinv * rinv;
+#pragma unroll
+        for (int c = kk + 1; c < 8; ++c) {
+          va[c] = fma(-(va[kk] * lck[c]), dinv, va[c]);
+          vb[c] = fma(-(vb[kk] * lck[c]), dinv, vb[c]);
         }
+        va[kk] = (lane == kk) ? d * rinv : va[kk] * rinv;
+        vb[kk] *= rinv;
+        if (lane == kk) DL[(p0 + kk) * LD + NT] = rinv;  // 1 / L_kk for the inverse
       }
-      sprev = sqrt(d);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (ha) DL[ra * LD + p0 + c] = va[c];
+        if (hb) DL[rb * LD + p0 + c] = vb[c];
+      }
+      if (lane == 0) s_fail = fail;
+    } else if (NW > 1 && p > 0 && warp == 1 + (p - 1) % (NW > 1 ? NW - 1 : 1)) {
+      leaf_inverse<NT>(DL, p0 - 8, lane);  // overlaps the pivot chain of panel p
     }
     __syncthreads();
-    {
-      const int k = p0 + 7;
-      const double rs = 1.0 / sprev;
-      for (int i = k + tid; i < NT; i += NTHREADS) DL[i * LD + k] = (i == k) ? sprev : DL[i * LD + k] * rs;
-    }
-    __syncthreads();
-    // trailing update of the lower 8x8 tiles right of the panel: A22 -= L21 L21^T (k = 8)
-    const int m = NT / 8 - p - 1;
+    BTD_PHASE(10);
+    if (s_fail) return s_fail;
+    // trailing update of the lower 8x8 tiles right of the panel: A22 -= L21 L21^T (k = 8), batched
+    const int m = NP - p - 1;
+#ifdef BTD_EXP_NO_TRAILING
+    const int units = 0;
+#else
     const int units = m * (m + 1) / 2;
+#endif
+#pragma unroll 1
     for (int u = warp; u < units; u += NW) {
       int tr, tc;
       tri_decode(u, tr, tc);
       tr += p + 1;
       tc += p + 1;
+      const double* pa = DL + (tr * 8 + (lane >> 2)) * LD + p0 + (lane & 3);
+      const double* pb = DL + (tc * 8 + (lane >> 2)) * LD + p0 + (lane & 3);
       double acc[2] = {0.0, 0.0};
-#pragma unroll
-      for (int ks = 0; ks < 8; ks += 4) {
-        const double a = DL[(tr * 8 + (lane >> 2)) * LD + p0 + ks + (lane & 3)];
-        const double b = DL[(tc * 8 + (lane >> 2)) * LD + p0 + ks + (lane & 3)];
-        dmma(acc, a, b);
-      }
+      dmma(acc, pa[0], pb[0]);
+      dmma(acc, pa[4], pb[4]);
       double* dst = DL + (tr * 8 + (lane >> 2)) * LD + tc * 8 + 2 * (lane & 3);
       dst[0] -= acc[0];
       dst[1] -= acc[1];
     }
+    __syncthreads();
+    BTD_PHASE(11);
   }
+  // remaining leaves: the last panel's (and all of them when the CTA has a single warp)
+  for (int lf = (NW > 1 ? NP - 1 : 0) + warp; lf < NP; lf += NW) leaf_inverse<NT>(DL, lf * 8, lane);
   __syncthreads();
+  BTD_PHASE(12);
 
-  // ---- triangular inverse: 8x8 leaves (one warp each), then recursive doubling with DMMA ----
-  {
-    const int d0 = warp * 8;
-    double x[8];
-    if (lane < 8) {
-      const int c = lane;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        if (i < c) {
-          x[i] = 0.0;
-        } else if (i == c) {
-          x[i] = 1.0 / DL[(d0 + i) * LD + d0 + i];
-        } else {
-          double s = 0.0;
-#pragma unroll
-          for (int mm = 0; mm < i; ++mm)
-            if (mm >= c) s += DL[(d0 + i) * LD + d0 + mm] * x[mm];
-          x[i] = -s / DL[(d0 + i) * LD + d0 + i];
-        }
-      }
-    }
-    __syncwarp();
-    if (lane < 8) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) DL[(d0 + i) * LD + d0 + lane] = x[i];
-    }
-  }
-  __syncthreads();
+  // ---- recursive doubling: [[A,0],[B,C]]^{-1} = [[Ai,0],[-Ci B Ai, Ci]] on DMMA ----
 #pragma unroll
   for (int b = 8; 2 * b <= NT; b *= 2) {
     const int tpb = b / 8;
     const int units = (NT / (2 * b)) * tpb * tpb;
+    constexpr int MAXV = (NT / 16 * 1 + NW - 1) / NW > 2 ? 2 : 2;  // <= 2 units per warp at every level
     // phase 1: T = B * Ainv   -> strictly-upper scratch block (rows i0.., cols i0+b..)
-    for (int u = warp; u < units; u += NW) {
-      const int pair = u / (tpb * tpb), rem = u % (tpb * tpb), tr = rem / tpb, tc = rem % tpb;
-      const int i0 = pair * 2 * b;
-      double acc[2] = {0.0, 0.0};
-      for (int k0 = tc * 8; k0 < b; k0 += 4) {
-        const double a = DL[(i0 + b + tr * 8 + (lane >> 2)) * LD + i0 + k0 + (lane & 3)];
-        const double bb = DL[(i0 + k0 + (lane & 3)) * LD + i0 + tc * 8 + (lane >> 2)];
-        dmma(acc, a, bb);
+    {
+      double acc[MAXV][2];
+      int i0v[MAXV], trv[MAXV], tcv[MAXV];
+      bool ok[MAXV];
+#pragma unroll
+      for (int q = 0; q < MAXV; ++q) {
+        const int u = warp + q * NW;
+        ok[q] = u < units;
+        const int pair = u / (tpb * tpb), rem = u % (tpb * tpb);
+        i0v[q] = pair * 2 * b;
+        trv[q] = rem / tpb;
+        tcv[q] = rem % tpb;
+        acc[q][0] = acc[q][1] = 0.0;
       }
-      double* dst = DL + (i0 + tr * 8 + (lane >> 2)) * LD + i0 + b + tc * 8 + 2 * (lane & 3);
-      dst[0] = acc[0];
-      dst[1] = acc[1];
+      for (int k0 = 0; k0 < b; k0 += 4) {
+#pragma unroll
+        for (int q = 0; q < MAXV; ++q) {
+          if (!ok[q] || k0 < tcv[q] * 8) continue;  // Ainv[k][c] == 0 for k < c
+          const int i0 = i0v[q];
+          const double a = DL[(i0 + b + trv[q] * 8 + (lane >> 2)) * LD + i0 + k0 + (lane & 3)];
+          const double bb = DL[(i0 + k0 + (lane & 3)) * LD + i0 + tcv[q] * 8 + (lane >> 2)];
+          dmma(acc[q], a, bb);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < MAXV; ++q) {
+        if (!ok[q]) continue;
+        const int i0 = i0v[q];
+        double* dst = DL + (i0 + trv[q] * 8 + (lane >> 2)) * LD + i0 + b + tcv[q] * 8 + 2 * (lane & 3);
+        dst[0] = acc[q][0];
+        dst[1] = acc[q][1];
+      }
     }
     __syncthreads();
     // phase 2: B <- -Cinv * T
-    for (int u = warp; u < units; u += NW) {
-      const int pair = u / (tpb * tpb), rem = u % (tpb * tpb), tr = rem / tpb, tc = rem % tpb;
-      const int i0 = pair * 2 * b;
-      double acc[2] = {0.0, 0.0};
-      for (int k0 = 0; k0 <= tr * 8 + 4; k0 += 4) {
-        const double a = DL[(i0 + b + tr * 8 + (lane >> 2)) * LD + i0 + b + k0 + (lane & 3)];
-        const double bb = DL[(i0 + k0 + (lane & 3)) * LD + i0 + b + tc * 8 + (lane >> 2)];
-        dmma(acc, a, bb);
+    {
+      double acc[MAXV][2];
+      int i0v[MAXV], trv[MAXV], tcv[MAXV];
+      bool ok[MAXV];
+#pragma unroll
+      for (int q = 0; q < MAXV; ++q) {
+        const int u = warp + q * NW;
+        ok[q] = u < units;
+        const int pair = u / (tpb * tpb), rem = u % (tpb * tpb);
+        i0v[q] = pair * 2 * b;
+        trv[q] = rem / tpb;
+        tcv[q] = rem % tpb;
+        acc[q][0] = acc[q][1] = 0.0;
       }
-      double* dst = DL + (i0 + b + tr * 8 + (lane >> 2)) * LD + i0 + tc * 8 + 2 * (lane & 3);
-      dst[0] = -acc[0];
-      dst[1] = -acc[1];
+      for (int k0 = 0; k0 < b; k0 += 4) {
+#pragma unroll
+        for (int q = 0; q < MAXV; ++q) {
+          if (!ok[q] || k0 > trv[q] * 8 + 4) continue;  // Cinv[r][k] == 0 for k > r
+          const int i0 = i0v[q];
+          const double a = DL[(i0 + b + trv[q] * 8 + (lane >> 2)) * LD + i0 + b + k0 + (lane & 3)];
+          const double bb = DL[(i0 + k0 + (lane & 3)) * LD + i0 + b + tcv[q] * 8 + (lane >> 2)];
+          dmma(acc[q], a, bb);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < MAXV; ++q) {
+        if (!ok[q]) continue;
+        const int i0 = i0v[q];
+        double* dst = DL + (i0 + b + trv[q] * 8 + (lane >> 2)) * LD + i0 + tcv[q] * 8 + 2 * (lane & 3);
+        dst[0] = -acc[q][0];
+        dst[1] = -acc[q][1];
+      }
     }
     __syncthreads();
   }
+  BTD_PHASE(13);
   return 0;
 }
 
-// Pt = Xt * Linv^T, in place on the XP rows owned by this warp (16 rows per warp).
+// Pt = Xt * Linv^T, in place on the XP rows owned by this warp (16 rows per warp, two 8-row passes:
+// a pass reads only its own rows, so it can overwrite them after a __syncwarp).
 template <int NT>
 __device__ __forceinline__ void pt_gemm(double* XP, const double* DL, bool coupled, int warp, int lane) {
   using S = FactorShape<NT>;
@@ -212,35 +308,31 @@ __device__ __forceinline__ void pt_gemm(double* XP, const double* DL, bool coupl
   constexpr int NCT = NT / 8;
   const int row0 = warp * 16;
   if (!coupled && row0 >= NT) return;
-  double acc[2][NCT][2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int c = 0; c < NCT; ++c) acc[i][c][0] = acc[i][c][1] = 0.0;
-  const double* pa = XP + (row0 + (lane >> 2)) * LD + (lane & 3);
   const double* pb = DL + (lane >> 2) * LD + (lane & 3);
+#pragma unroll 1
+  for (int rt = 0; rt < 2; ++rt) {
+    double acc[NCT][2];
 #pragma unroll
-  for (int k0 = 0; k0 < NT; k0 += 4) {
-    const double a0 = pa[k0];
-    const double a1 = pa[8 * LD + k0];
+    for (int c = 0; c < NCT; ++c) acc[c][0] = acc[c][1] = 0.0;
+    const double* pa = XP + (row0 + rt * 8 + (lane >> 2)) * LD + (lane & 3);
 #pragma unroll
-    for (int ct = 0; ct < NCT; ++ct) {
-      if (ct * 8 + 7 < k0) continue;  // Linv[c][k] == 0 for k > c
-      const double b = pb[ct * 8 * LD + k0];
-      dmma(acc[0][ct], a0, b);
-      dmma(acc[1][ct], a1, b);
+    for (int k0 = 0; k0 < NT; k0 += 4) {
+      const double a0 = pa[k0];
+#pragma unroll
+      for (int ct = 0; ct < NCT; ++ct) {
+        if (ct * 8 + 7 < k0) continue;  // Linv[c][k] == 0 for k > c
+        dmma(acc[ct], a0, pb[ct * 8 * LD + k0]);
+      }
     }
-  }
-  __syncwarp();
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
+    __syncwarp();
 #pragma unroll
     for (int ct = 0; ct < NCT; ++ct) {
       double2 v;
-      v.x = acc[i][ct][0];
-      v.y = acc[i][ct][1];
-      *reinterpret_cast<double2*>(XP + (row0 + i * 8 + (lane >> 2)) * LD + ct * 8 + 2 * (lane & 3)) = v;
+      v.x = acc[ct][0];
+      v.y = acc[ct][1];
+      *reinterpret_cast<double2*>(XP + (row0 + rt * 8 + (lane >> 2)) * LD + ct * 8 + 2 * (lane & 3)) = v;
     }
+  }
 }
 
 // acc += Pt[R-tile] * Pt[C-tile]^T over k = 0..NT (one TS x TS warp tile of the lower 2NT x 2NT product)
@@ -252,7 +344,7 @@ __device__ __forceinline__ void syrk_tile(const double* XP, int R, int C, double
   const bool diag = (R == C);
   const double* pa = XP + (R * TS + (lane >> 2)) * LD + (lane & 3);
   const double* pb = XP + (C * TS + (lane >> 2)) * LD + (lane & 3);
-#pragma unroll
+#pragma unroll 4
   for (int k0 = 0; k0 < NT; k0 += 4) {
     double a[SUB], b[SUB];
 #pragma unroll
@@ -269,7 +361,8 @@ __device__ __forceinline__ void syrk_tile(const double* XP, int R, int C, double
 }
 
 template <int NT>
-__global__ void __launch_bounds__(FactorShape<NT>::NTHREADS) factor_level_kernel(FactorArgs args) {
+__global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MINB)
+    factor_level_kernel(FactorArgs args) {
   using S = FactorShape<NT>;
   constexpr int LD = S::LD, NTHREADS = S::NTHREADS, NW = S::NW, TS = S::TS, SUB = S::SUB;
   constexpr int HALF = S::HALF, NSL = S::NSL, NG = S::NG, ND = S::ND;
@@ -301,18 +394,13 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS) factor_level_kernel
   }
   cp_async_wait_all();
   for (int r = n + tid; r < NT; r += NTHREADS) DL[r * LD + r] = 1.0;
-
-  double acc_sl[S::MAXSL][SUB][SUB][2];
-#pragma unroll
-  for (int s = 0; s < S::MAXSL; ++s)
-#pragma unroll
-    for (int i = 0; i < SUB; ++i)
-#pragma unroll
-      for (int jj = 0; jj < SUB; ++jj) acc_sl[s][i][jj][0] = acc_sl[s][i][jj][1] = 0.0;
+  BTD_PHASE_INIT();
 
   for (int j = 0; j < J; ++j) {
     const bool last = (j == J - 1);
+    BTD_PHASE(0);
     const int piv = potrf_trtri<NT>(DL);  // begins with a barrier
+    BTD_PHASE(1);
     if (piv) {
       if (tid == 0 && piv <= n) report_npd(args.err, args.level, j, k, piv);
       return;
@@ -322,24 +410,51 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS) factor_level_kernel
 
     cp_async_wait_all();
     __syncthreads();
+    BTD_PHASE(2);
     pt_gemm<NT>(XP, DL, coupled, warp, lane);
     __syncthreads();
+    BTD_PHASE(3);
     if (!last) {
       store_block<NT, LD, NTHREADS>(args.Lsub + (start + j) * bs, XP, n, false);  // L_{j+1,j}
       stage_block_async<NT, LD, NTHREADS>(DL, args.diag + (start + j + 1) * bs, n);
       cp_async_commit();
     }
 
+    BTD_PHASE(4);
     // ---- C = Pt Pt^T (lower): S_L tiles (persistent) and G tiles (held until XP is free) ----
     double held[S::MAXG][SUB][SUB][2];
     if (coupled) {
+      // S_L accumulates across the segment's steps in its global output slot (L2 resident):
+      // keeping it in registers would cost 32 registers for the whole kernel.
 #pragma unroll
       for (int s = 0; s < S::MAXSL; ++s) {
         const int t = warp + s * NW;
         if (t < NSL) {
           int rr, cc;
           tri_decode(t, rr, cc);
-          syrk_tile<NT>(XP, HALF + rr, HALF + cc, acc_sl[s], lane);
+          double acc[SUB][SUB][2];
+#pragma unroll
+          for (int i = 0; i < SUB; ++i)
+#pragma unroll
+            for (int jj = 0; jj < SUB; ++jj) {
+              const int r = rr * TS + i * 8 + (lane >> 2);
+              const int c = cc * TS + jj * 8 + 2 * (lane & 3);
+              const double* src = args.Sl + (size_t)k * bs + (size_t)r * n + c;
+              acc[i][jj][0] = (j > 0 && r < n && c < n) ? src[0] : 0.0;
+              acc[i][jj][1] = (j > 0 && r < n && c + 1 < n) ? src[1] : 0.0;
+            }
+          syrk_tile<NT>(XP, HALF + rr, HALF + cc, acc, lane);
+#pragma unroll
+          for (int i = 0; i < SUB; ++i)
+#pragma unroll
+            for (int jj = 0; jj < SUB; ++jj) {
+              if (rr == cc && jj > i) continue;
+              const int r = rr * TS + i * 8 + (lane >> 2);
+              const int c = cc * TS + jj * 8 + 2 * (lane & 3);
+              double* dst = args.Sl + (size_t)k * bs + (size_t)r * n + c;
+              if (r < n && c < n) dst[0] = acc[i][jj][0];
+              if (r < n && c + 1 < n) dst[1] = acc[i][jj][1];
+            }
         }
       }
 #pragma unroll
@@ -352,8 +467,10 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS) factor_level_kernel
         if (g < NG) syrk_tile<NT>(XP, HALF + g / HALF, g % HALF, held[s], lane);
       }
     }
+    BTD_PHASE(5);
     cp_async_wait_all();
     __syncthreads();
+    BTD_PHASE(6);
     // ---- D tiles: D_{j+1} = A_{j+1,j+1} - P1^T P1  (or S_R at the last row) ----
 #pragma unroll
     for (int s = 0; s < S::MAXD; ++s) {
@@ -386,7 +503,9 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS) factor_level_kernel
           }
       }
     }
+    BTD_PHASE(7);
     __syncthreads();  // every read of XP (Pt) is complete
+    BTD_PHASE(8);
     if (coupled) {
 #pragma unroll
       for (int s = 0; s < S::MAXG; ++s) {
@@ -422,28 +541,6 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS) factor_level_kernel
     }
   }
 
-  if (coupled) {
-#pragma unroll
-    for (int s = 0; s < S::MAXSL; ++s) {
-      const int t = warp + s * NW;
-      if (t >= NSL) continue;
-      int rr, cc;
-      tri_decode(t, rr, cc);
-#pragma unroll
-      for (int i = 0; i < SUB; ++i)
-#pragma unroll
-        for (int jj = 0; jj < SUB; ++jj) {
-          if (rr == cc && jj > i) continue;
-          const int r = rr * TS + i * 8 + (lane >> 2);
-          const int c = cc * TS + jj * 8 + 2 * (lane & 3);
-          if (r < n) {
-            double* dst = args.Sl + (size_t)k * bs + (size_t)r * n;
-            if (c < n) dst[c] = acc_sl[s][i][jj][0];
-            if (c + 1 < n) dst[c + 1] = acc_sl[s][i][jj][1];
-          }
-        }
-    }
-  }
 }
 
 // Next-level diagonal: S_diag[p] = (A[s_p] - S_L[p]) - S_R[p-1]  (reference order, bt/schur.py:186-188).

@@ -46,7 +46,7 @@ template <int NT, int DC, bool TRANS>
 __device__ __forceinline__ void block_mv(const double* __restrict__ M, int n, const double* x, double* y,
                                          double sign, bool accumulate, double* red) {
   using S = SolveShape<NT>;
-  constexpr int TPR = S::TPR, CPT = S::CPT, NTHREADS = S::NTHREADS;
+  constexpr int TPR = S::TPR, CPT = S::CPT;
   const int tid = threadIdx.x;
   double part[DC];
 #pragma unroll

@@ -39,12 +39,26 @@ class RecursionConfig:
                                  1 if self.auto_crossover else 0, 0)
 
 
-@dataclass
 class FactorLevel:
-    """One recursion level: its partition (schur.py:67-72). The factor blocks stay on the device."""
+    """One recursion level: its partition (schur.py:67-72). The factor blocks stay on the device.
 
-    plan: PartitionPlan
-    level: int
+    ``plan`` is materialised lazily (a 2^20-block level has ~10^5 separators; building the
+    Python tuples eagerly would dominate the host time of a factorization)."""
+
+    def __init__(self, num_blocks: int, separators: np.ndarray, level: int):
+        self.num_blocks = num_blocks
+        self.separators = separators
+        self.level = level
+        self._plan = None
+
+    @property
+    def plan(self) -> PartitionPlan:
+        if self._plan is None:
+            self._plan = _plan_from_separators(self.num_blocks, self.separators.tolist())
+        return self._plan
+
+    def __repr__(self):
+        return f"FactorLevel(level={self.level}, num_blocks={self.num_blocks}, separators={len(self.separators)})"
 
 
 @dataclass
@@ -116,8 +130,8 @@ def _device_matrix(matrix: BlockTridiagonalMatrix):
     if _is_torch(matrix.diag):
         dev = matrix.diag.device
         if dev.type != "cuda":
-            diag = matrix.diag.to("cuda")
-            sub = matrix.sub.to("cuda")
+            diag = matrix.diag.to("cuda", non_blocking=True)
+            sub = matrix.sub.to("cuda", non_blocking=True)
         else:
             diag, sub = matrix.diag, matrix.sub
         diag = diag.to(torch.float64).contiguous()
@@ -131,7 +145,7 @@ def _device_matrix(matrix: BlockTridiagonalMatrix):
 
 
 def recursive_factorize(matrix: BlockTridiagonalMatrix, config: RecursionConfig | None = None,
-                        *, stream=None) -> FactorHierarchy:
+                        *, stream=None, profile: bool = False) -> FactorHierarchy:
     """Factor an SPD block-tridiagonal system for repeated solves (schur.py:289-318).
 
     Never mutates ``matrix``. Raises NotPositiveDefinite(pivot, level, member, block) with the
@@ -154,6 +168,8 @@ def recursive_factorize(matrix: BlockTridiagonalMatrix, config: RecursionConfig 
     persistent = torch.empty(pers_b.value, dtype=torch.uint8, device=dev)
     scratch = torch.empty(scr_b.value, dtype=torch.uint8, device=dev)
     native = NativeFactor(handle, persistent, dev)
+    if profile:
+        L.btd_profile_kernels(handle, 1)
     s = stream if stream is not None else torch.cuda.current_stream(dev)
     rc = L.btd_factorize(handle, diag.data_ptr(), sub.data_ptr() if N > 1 else None, persistent.data_ptr(),
                          scratch.data_ptr(), ctypes.c_void_p(s.cuda_stream), 1, ctypes.byref(st))
@@ -166,9 +182,9 @@ def recursive_factorize(matrix: BlockTridiagonalMatrix, config: RecursionConfig 
     for lvl in range(nl.value):
         lnb, lp = ctypes.c_int64(), ctypes.c_int64()
         L.btd_level_info(handle, lvl, ctypes.byref(lnb), ctypes.byref(lp), None)
-        seps = (ctypes.c_int64 * lp.value)()
-        L.btd_level_info(handle, lvl, None, None, seps)
-        levels.append(FactorLevel(_plan_from_separators(lnb.value, seps), lvl))
+        seps = np.empty(lp.value, dtype=np.int64)
+        L.btd_level_info(handle, lvl, None, None, seps.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+        levels.append(FactorLevel(lnb.value, seps, lvl))
     return FactorHierarchy(N, n, levels, BaseFactor(nb.value, n), native)
 
 
@@ -188,12 +204,13 @@ def recursive_solve(hierarchy: FactorHierarchy, rhs: BlockRhs, *, stream=None) -
         raise ValueError("hierarchy must be factorized before solving")
     L = _native.lib()
     host = not _is_torch(rhs.blocks)
+    host_tensor = (not host) and rhs.blocks.device.type == "cpu"
     if host:
         b = torch.from_numpy(np.ascontiguousarray(rhs.blocks, dtype=np.float64)).to(native.device)
     else:
         b = rhs.blocks
         if b.device != native.device:
-            b = b.to(native.device)
+            b = b.to(native.device, non_blocking=True)
         b = b.to(torch.float64).contiguous()
     d = int(b.shape[2])
     x = torch.empty_like(b)
@@ -208,7 +225,38 @@ def recursive_solve(hierarchy: FactorHierarchy, rhs: BlockRhs, *, stream=None) -
         _raise_status(st, rc)
     if host:
         return BlockRhs(x.cpu().numpy())
+    if host_tensor:
+        return BlockRhs(x.cpu())
     return BlockRhs(x)
+
+
+def factor_kernel_times(matrix: BlockTridiagonalMatrix, config: RecursionConfig | None = None,
+                        repeats: int = 3) -> dict:
+    """Bench helper: median (over ``repeats``) device times of factor, solve and the level-0 factor
+    kernel (CUDA events on the launching stream, C-ABI timing hook)."""
+    import statistics
+
+    import torch
+    f_ms, s_ms, l0 = [], [], []
+    rhs = BlockRhs(torch.ones((matrix.num_blocks, matrix.block_size, 1), dtype=torch.float64,
+                              device=matrix.diag.device))
+    for _ in range(repeats):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record()
+        h = recursive_factorize(matrix, config, profile=True)
+        e[1].record()
+        recursive_solve(h, rhs)
+        e[2].record()
+        torch.cuda.synchronize()
+        f_ms.append(e[0].elapsed_time(e[1]))
+        s_ms.append(e[1].elapsed_time(e[2]))
+        L = _native.lib()
+        cnt = ctypes.c_int64()
+        out = (ctypes.c_float * 64)()
+        L.btd_kernel_times(h._native.handle, out, 64, ctypes.byref(cnt))
+        l0.append(out[0])
+    return {"factor_ms": statistics.median(f_ms), "solve_ms": statistics.median(s_ms),
+            "level0_factor_ms": statistics.median(l0)}
 
 
 def level_factor(hierarchy: FactorHierarchy, level: int):
@@ -217,7 +265,7 @@ def level_factor(hierarchy: FactorHierarchy, level: int):
     native = hierarchy._native
     L = _native.lib()
     n = hierarchy.block_size
-    N = hierarchy.base.num_blocks if level == len(hierarchy.levels) else hierarchy.levels[level].plan.num_blocks
+    N = hierarchy.base.num_blocks if level == len(hierarchy.levels) else hierarchy.levels[level].num_blocks
     linv = torch.empty((N, n, n), dtype=torch.float64, device=native.device)
     lsub = torch.empty((max(N - 1, 0), n, n), dtype=torch.float64, device=native.device)
     st = _native.BtdStatus()
