@@ -13,6 +13,7 @@
 
 #include "btd_factor.cuh"
 #include "btd_solve.cuh"
+#include "btd_solve2.cuh"
 
 namespace {
 
@@ -160,6 +161,55 @@ cudaError_t dispatch_solve_dc(const btd::SolveArgs& a, unsigned grid_x, cudaStre
   return launch_solve<NT, 4>(a, grid_x, s);
 }
 
+template <int NT, int DC>
+cudaError_t launch_stream(const btd::SolveArgs& a, cudaStream_t s) {
+  using S = btd::Solve2Shape<NT>;
+  constexpr size_t smem = sizeof(double) * ((size_t)S::STAGES * (S::FULL + S::PACK + NT * DC) +
+                                            (size_t)(4 + S::ZMAX + S::PARTS) * NT * DC);
+  static int blocks_per_sm = -1, sms = 0;
+  if (blocks_per_sm < 0) {
+    cudaError_t e = cudaFuncSetAttribute(btd::solve_stream_kernel<NT, DC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, btd::solve_stream_kernel<NT, DC>,
+                                                      S::NTHREADS, smem);
+    if (e != cudaSuccess) return e;
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  const long long cap = (long long)blocks_per_sm * sms;
+  const unsigned gx = (unsigned)(a.K < cap ? a.K : cap);
+  dim3 grid(gx, (unsigned)((a.d + DC - 1) / DC));
+  btd::solve_stream_kernel<NT, DC><<<grid, S::NTHREADS, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int NT>
+cudaError_t dispatch_stream_dc(const btd::SolveArgs& a, cudaStream_t s) {
+  if (a.d == 1) return launch_stream<NT, 1>(a, s);
+  if (a.d == 2) return launch_stream<NT, 2>(a, s);
+  return launch_stream<NT, 4>(a, s);
+}
+
+cudaError_t dispatch_stream(int nt, const btd::SolveArgs& a, cudaStream_t s) {
+  switch (nt) {
+    case 8: return dispatch_stream_dc<8>(a, s);
+    case 16: return dispatch_stream_dc<16>(a, s);
+    case 32: return dispatch_stream_dc<32>(a, s);
+    case 64: return dispatch_stream_dc<64>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// longest interior segment of a level (the streaming solve caches z for segments up to ZMAX)
+int64_t max_segment(const LevelPlan& lp) {
+  int64_t m = 0;
+  for (int64_t k = 0; k < lp.K; ++k) m = std::max(m, lp.seps[k + 1] - lp.seps[k] - 1);
+  return m;
+}
+
 cudaError_t dispatch_solve(int nt, const btd::SolveArgs& a, unsigned grid_x, cudaStream_t s) {
   switch (nt) {
     case 8: return dispatch_solve_dc<8>(a, grid_x, s);
@@ -274,6 +324,7 @@ int btd_create(int64_t num_blocks, int64_t block_size, const btd_config* cfg, bt
   h->cfg = *cfg;
   h->nt = nt;
   const size_t bb = (size_t)block_size * block_size * sizeof(double);
+  const size_t pb = (size_t)btd::packed_stride((int)block_size) * sizeof(double);
 
   // ---- recursion plan (recursive_factorize level loop, bt/schur.py:298-318) ----
   int64_t cur = num_blocks;
@@ -309,13 +360,13 @@ int btd_create(int64_t num_blocks, int64_t block_size, const btd_config* cfg, bt
     lp.off_seps = off;
     off = align_up(off + (size_t)lp.P * sizeof(int));
     lp.off_linv = off;
-    off = align_up(off + (size_t)lp.N * bb);
+    off = align_up(off + (size_t)lp.N * pb);
     lp.off_lsub = off;
     off = align_up(off + (size_t)(lp.N - 1) * bb);
   }
   if (!h->overflow) {
     h->off_base_linv = off;
-    off = align_up(off + (size_t)h->base_N * bb);
+    off = align_up(off + (size_t)h->base_N * pb);
     h->off_base_lsub = off;
     off = align_up(off + (size_t)std::max<int64_t>(h->base_N - 1, 1) * bb);
   }
@@ -518,7 +569,7 @@ int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, v
     a.K = (int)lp.K;
     a.mode = btd::kSolveDown;
     a.err = err;
-    e = dispatch_solve(h->nt, a, (unsigned)lp.K, stream);
+    e = h->nt >= 32 ? dispatch_stream(h->nt, a, stream) : dispatch_solve(h->nt, a, (unsigned)lp.K, stream);
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(down)");
     btd::assemble_separator_rhs_kernel<<<(unsigned)lp.P, 128, 0, stream>>>(rhs_l[l], a.seps, rhs_l[l + 1], fr_l[l],
                                                                             (int)lp.K, n, (int)d, err);
@@ -555,7 +606,7 @@ int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, v
     a.K = (int)lp.K;
     a.mode = btd::kSolveUp;
     a.err = err;
-    e = dispatch_solve(h->nt, a, (unsigned)lp.K, stream);
+    e = h->nt >= 32 ? dispatch_stream(h->nt, a, stream) : dispatch_solve(h->nt, a, (unsigned)lp.K, stream);
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(up)");
   }
   return BTD_OK;
@@ -582,7 +633,8 @@ int btd_level_factor(const btd_hierarchy* h, int64_t level, double* linv_out, do
   }
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
-  if (linv_out) e = cudaMemcpyAsync(linv_out, h->persistent + ol, (size_t)N * bb, cudaMemcpyDeviceToDevice, s);
+  const size_t pb = (size_t)btd::packed_stride((int)h->n) * sizeof(double);
+  if (linv_out) e = cudaMemcpyAsync(linv_out, h->persistent + ol, (size_t)N * pb, cudaMemcpyDeviceToDevice, s);
   if (e == cudaSuccess && lsub_out && N > 1)
     e = cudaMemcpyAsync(lsub_out, h->persistent + os, (size_t)(N - 1) * bb, cudaMemcpyDeviceToDevice, s);
   if (e != cudaSuccess) return cuda_fail(st, e, "btd_level_factor");

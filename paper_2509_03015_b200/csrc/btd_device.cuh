@@ -62,6 +62,10 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 // Stage an n x n row-major global block into an NT x LD shared tile, zero-padding rows/cols >= n.
 template <int NT, int LD, int NTHREADS>
@@ -121,6 +125,23 @@ __device__ __forceinline__ void store_block(double* g, const double* sm, int n, 
     for (int idx = threadIdx.x; idx < n * n; idx += NTHREADS) {
       const int r = idx / n, c = idx % n;
       g[(size_t)r * n + c] = (lower_only && c > r) ? 0.0 : sm[r * LD + c];
+    }
+  }
+}
+
+// Store the lower triangle of the n x n leading part of a shared tile in packed row-major form
+// (row r at offset r(r+1)/2): the inverse Cholesky factors are stored this way.
+template <int NT, int LD, int NTHREADS>
+__device__ __forceinline__ void store_packed_lower(double* g, const double* sm, int n) {
+  if (n == NT) {
+    for (int e = threadIdx.x; e < NT * NT; e += NTHREADS) {
+      const int r = e / NT, c = e % NT;
+      if (c <= r) g[r * (r + 1) / 2 + c] = sm[r * LD + c];
+    }
+  } else {
+    for (int e = threadIdx.x; e < n * n; e += NTHREADS) {
+      const int r = e / n, c = e % n;
+      if (c <= r) g[r * (r + 1) / 2 + c] = sm[r * LD + c];
     }
   }
 }

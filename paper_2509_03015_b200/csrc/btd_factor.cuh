@@ -50,7 +50,8 @@ struct FactorArgs {
   int K;        // segments (base: 1)
   int base;     // 1: serial base case, the whole chain is one uncoupled segment
   int level;
-  double* Linv;  // (N, n, n) out: inverse Cholesky factor of every interior row
+  double* Linv;  // (N, packed) out: inverse Cholesky factor of every interior row, packed lower
+                 // triangle (row r at r(r+1)/2), block stride n(n+1)/2 rounded up to even
   double* Lsub;  // (N-1, n, n) out: L_{i,i-1} inside segments; coupling copies at segment edges
   double* Sl;    // (K, n, n) out: S_L per segment (written into the next level's diag slots)
   double* Sr;    // (K, n, n) out: S_R per segment
@@ -63,21 +64,30 @@ struct FactorShape {
   static constexpr int LD = NT + 4;  // +4 doubles: conflict-free DMMA fragment loads
   static constexpr int NTHREADS = NT == 64 ? 256 : NT == 32 ? 128 : NT == 16 ? 64 : 32;
   static constexpr int NW = NTHREADS / 32;
+  // warp specialisation: group A (warps [0, NWA)) factors the diagonal block, group B
+  // (warps [NWA, NW)) finishes the previous step's Schur/fill updates concurrently.
+  static constexpr int NWA = NW >= 2 ? NW / 2 : 1;
+  static constexpr int NWB = NW - NWA;
   static constexpr int TS = NT == 8 ? 8 : 16;  // syrk warp tile
   static constexpr int SUB = TS / 8;
   static constexpr int TSR = 2 * NT / TS;
   static constexpr int HALF = TSR / 2;
   static constexpr int NSL = HALF * (HALF + 1) / 2;
-  static constexpr int NG = HALF * HALF;
   static constexpr int ND = NSL;
-  static constexpr int MAXSL = (NSL + NW - 1) / NW;
-  static constexpr int MAXG = (NG + NW - 1) / NW;
   static constexpr int MAXD = (ND + NW - 1) / NW;
+  static constexpr int MAXV = (NT * NT / 256 + NWA - 1) / NWA > 0 ? (NT * NT / 256 + NWA - 1) / NWA : 1;
   static constexpr size_t SMEM = (size_t)3 * NT * LD * sizeof(double);
   static constexpr int MINB = NT == 64 ? 2 : NT == 32 ? 4 : 8;  // CTAs per SM to overlap pivot latency
   static_assert(NT / 8 == NW, "one trtri leaf per warp");
-  static_assert(NTHREADS == 4 * NT, "potrf thread map: 8 panel columns x NT/2 row pairs");
+  static_assert(NWB == 0 || 16 * NWB == NT, "group B owns 16 rows of the fill block per warp");
 };
+
+constexpr int kBarA = 1;  // named barrier of group A
+constexpr int kBarB = 2;  // named barrier of group B
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 __device__ __forceinline__ void tri_decode(int s, int& r, int& c) {
   r = 0;
@@ -120,118 +130,154 @@ __device__ __forceinline__ void leaf_inverse(double* DL, int d0, int lane) {
   }
 }
 
+// One 8-column panel of the Cholesky factorization, factored by a single warp in registers
+// (lane l owns panel rows p0+l and, when HASB, p0+l+32).  The pivot chain is latency bound
+// (shfl -> rsqrt -> fma per column); it is software-pipelined so that the next column's pivot and
+// multipliers are shuffled right after that column's own update, ahead of the other updates.
+// Branch-free: a data-dependent `break` costs ~40% of the chain (tools/panel_bench.cu); a failed
+// pivot only poisons values that are discarded.  Returns the 1-based failing pivot or 0.
+template <int NT, bool HASB>
+__device__ __forceinline__ int panel_chain(double* DL, int p0, int lane) {
+  constexpr int LD = FactorShape<NT>::LD;
+  const int ra = p0 + lane, rb = p0 + lane + 32;
+  const bool ha = ra < NT, hb = HASB && rb < NT;
+  double va[8], vb[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    va[c] = ha ? DL[ra * LD + p0 + c] : 0.0;
+    vb[c] = hb ? DL[rb * LD + p0 + c] : 0.0;
+  }
+  int fail = 0;
+  double d = __shfl_sync(0xffffffffu, va[0], 0);
+  double lck[8];
+#pragma unroll
+  for (int c = 1; c < 8; ++c) lck[c] = __shfl_sync(0xffffffffu, va[0], c);
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    double t[8], u[8];
+#pragma unroll
+    for (int c = kk + 1; c < 8; ++c) {  // multipliers, ready before the pivot root
+      t[c] = va[kk] * lck[c];
+      if (HASB) u[c] = vb[kk] * lck[c];
+    }
+    fail = (fail == 0 && d <= 0.0) ? p0 + kk + 1 : fail;
+    const double rinv = rsqrt(d);
+    const double dinv = rinv * rinv;
+    double nd = 0.0, nl[8];
+    if (kk + 1 < 8) {
+      va[kk + 1] = fma(-t[kk + 1], dinv, va[kk + 1]);
+      if (HASB) vb[kk + 1] = fma(-u[kk + 1], dinv, vb[kk + 1]);
+      nd = __shfl_sync(0xffffffffu, va[kk + 1], kk + 1);
+#pragma unroll
+      for (int c = kk + 2; c < 8; ++c) nl[c] = __shfl_sync(0xffffffffu, va[kk + 1], c);
+    }
+#pragma unroll
+    for (int c = kk + 2; c < 8; ++c) {
+      va[c] = fma(-t[c], dinv, va[c]);
+      if (HASB) vb[c] = fma(-u[c], dinv, vb[c]);
+    }
+    va[kk] *= rinv;  // row p0+kk: d * rinv = sqrt(d)
+    if (HASB) vb[kk] *= rinv;
+    if (lane == kk) DL[(p0 + kk) * LD + NT] = rinv;  // 1 / L_kk for the inverse
+    d = nd;
+#pragma unroll
+    for (int c = kk + 2; c < 8; ++c) lck[c] = nl[c];
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (ha) DL[ra * LD + p0 + c] = va[c];
+    if (hb) DL[rb * LD + p0 + c] = vb[c];
+  }
+  return fail;
+}
+
+// rank-8 update of one 8x8 tile (tr, tc) by panel p: A[tr][tc] -= L[tr][p] L[tc][p]^T
+template <int NT>
+__device__ __forceinline__ void tile_update(double* DL, int tr, int tc, int p0, int lane) {
+  constexpr int LD = FactorShape<NT>::LD;
+  const double* pa = DL + (tr * 8 + (lane >> 2)) * LD + p0 + (lane & 3);
+  const double* pb = DL + (tc * 8 + (lane >> 2)) * LD + p0 + (lane & 3);
+  double acc[2] = {0.0, 0.0};
+  dmma(acc, pa[0], pb[0]);
+  dmma(acc, pa[4], pb[4]);
+  double* dst = DL + (tr * 8 + (lane >> 2)) * LD + tc * 8 + 2 * (lane & 3);
+  dst[0] -= acc[0];
+  dst[1] -= acc[1];
+}
+
 // ------------------------------------------------------------------------------------------
-// In-place Cholesky + triangular inverse of the NT x NT tile DL (lower triangle is read).
-// Returns the 1-based first non-positive pivot (reference _first_bad_pivot, bt/kernels.py:136-152;
-// failure test is `pivot <= 0` like the LAPACK/OpenBLAS path, so NaN propagates silently, SURVEY
-// §5), or 0.  The result is uniform across the CTA.
+// In-place Cholesky + triangular inverse of the NT x NT tile DL (lower triangle is read), run by
+// the NWA warps of group A (named barrier kBarA).  Returns the 1-based first non-positive pivot
+// (reference _first_bad_pivot, bt/kernels.py:136-152; failure test is `pivot <= 0` like the
+// LAPACK/OpenBLAS path, so NaN propagates silently), or 0 -- uniform over group A.
 //
-// Panel-blocked right-looking Cholesky.  Each 8-column panel is factored by ONE warp in
-// registers (lane l owns panel rows p0+l and p0+l+32): the pivot chain is latency bound
-// (shfl -> rsqrt -> fma per column), so it is kept short in instructions and leaves the issue
-// slots to the co-resident CTA.  While warp 0 factors panel p, another warp inverts the
-// 8x8 diagonal tile of panel p-1 (trtri leaf).  The trailing update of the lower 8x8 tiles is a
-// batched DMMA rank-8 update by all warps; the inverse is finished by recursive doubling on DMMA.
+// Panel-blocked right-looking Cholesky with look-ahead: warp 0 factors panel p (panel_chain)
+// while the other warps of the group apply panel p-1's update to the column blocks >= p+1 and
+// invert panel p-1's 8x8 diagonal tile (trtri leaf).  Only the update of column block p+1 by
+// panel p sits between two pivot chains.  The inverse is finished by recursive doubling on DMMA.
 // ------------------------------------------------------------------------------------------
 template <int NT>
-__device__ int potrf_trtri(double* DL) {
+__device__ int potrf_trtri(double* DL, int* s_fail) {
   using S = FactorShape<NT>;
   constexpr int LD = S::LD;
-  constexpr int NW = S::NW;
+  constexpr int NWA = S::NWA;
   constexpr int NP = NT / 8;
+  constexpr int MAXV = S::MAXV;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  __shared__ int s_fail;
   BTD_PHASE_INIT();
-  __syncthreads();
 
   for (int p = 0; p < NP; ++p) {
     const int p0 = p * 8;
     if (warp == 0) {
-      const int ra = p0 + lane, rb = p0 + lane + 32;
-      const bool ha = ra < NT, hb = rb < NT;
-      double va[8], vb[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        va[c] = ha ? DL[ra * LD + p0 + c] : 0.0;
-        vb[c] = hb ? DL[rb * LD + p0 + c] : 0.0;
+      const int f = (p0 + 32 < NT) ? panel_chain<NT, true>(DL, p0, lane) : panel_chain<NT, false>(DL, p0, lane);
+      if (lane == 0) *s_fail = f;
+    } else if (p > 0) {
+      // helpers: leaf of panel p-1, and panel p-1's update of the column blocks >= p+1
+      if (warp == 1 + (p - 1) % (NWA > 1 ? NWA - 1 : 1)) leaf_inverse<NT>(DL, p0 - 8, lane);
+      const int m = NP - p - 1;  // column blocks p+1 .. NP-1
+      const int units = m * (m + 1) / 2;
+      for (int u = warp - 1; u < units; u += NWA - 1) {
+        int tr, tc;
+        tri_decode(u, tr, tc);
+        tile_update<NT>(DL, tr + p + 1, tc + p + 1, p0 - 8, lane);
       }
-      // Branch-free pivot chain: a data-dependent `break` here costs ~40% of the chain latency
-      // (measured, tools/panel_bench.cu); a failed pivot only poisons values that are discarded.
-      int fail = 0;
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const double d = __shfl_sync(0xffffffffu, va[kk], kk);
-        double lck[8];
-#pragma unroll
-        for (int c = kk + 1; c < 8; ++c) lck[c] = __shfl_sync(0xffffffffu, va[kk], c);
-        fail = (fail == 0 && d <= 0.0) ? p0 + kk + 1 : fail;
-        const double rinv = rsqrt(d);
-        const double dinv = rinv * rinv;
-#pragma unroll
-        for (int c = kk + 1; c < 8; ++c) {
-          va[c] = fma(-(va[kk] * lck[c]), dinv, va[c]);
-          vb[c] = fma(-(vb[kk] * lck[c]), dinv, vb[c]);
-        }
-        va[kk] = (lane == kk) ? d * rinv : va[kk] * rinv;
-        vb[kk] *= rinv;
-        if (lane == kk) DL[(p0 + kk) * LD + NT] = rinv;  // 1 / L_kk for the inverse
-      }
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        if (ha) DL[ra * LD + p0 + c] = va[c];
-        if (hb) DL[rb * LD + p0 + c] = vb[c];
-      }
-      if (lane == 0) s_fail = fail;
-    } else if (NW > 1 && p > 0 && warp == 1 + (p - 1) % (NW > 1 ? NW - 1 : 1)) {
-      leaf_inverse<NT>(DL, p0 - 8, lane);  // overlaps the pivot chain of panel p
     }
-    __syncthreads();
-    BTD_PHASE(10);
-    if (s_fail) return s_fail;
-    // trailing update of the lower 8x8 tiles right of the panel: A22 -= L21 L21^T (k = 8), batched
-    const int m = NP - p - 1;
-#ifdef BTD_EXP_NO_TRAILING
-    const int units = 0;
-#else
-    const int units = m * (m + 1) / 2;
-#endif
-#pragma unroll 1
-    for (int u = warp; u < units; u += NW) {
-      int tr, tc;
-      tri_decode(u, tr, tc);
-      tr += p + 1;
-      tc += p + 1;
-      const double* pa = DL + (tr * 8 + (lane >> 2)) * LD + p0 + (lane & 3);
-      const double* pb = DL + (tc * 8 + (lane >> 2)) * LD + p0 + (lane & 3);
-      double acc[2] = {0.0, 0.0};
-      dmma(acc, pa[0], pb[0]);
-      dmma(acc, pa[4], pb[4]);
-      double* dst = DL + (tr * 8 + (lane >> 2)) * LD + tc * 8 + 2 * (lane & 3);
-      dst[0] -= acc[0];
-      dst[1] -= acc[1];
+    named_sync(kBarA, NWA * 32);
+    BTD_PHASE(4);
+    const int fail = *s_fail;
+    if (fail) return fail;
+    // critical: panel p's update of column block p+1 (tiles (tr, p+1), tr >= p+1)
+    for (int tr = p + 1 + warp; tr < NP; tr += NWA) tile_update<NT>(DL, tr, p + 1, p0, lane);
+    if (NWA == 1) {  // no helpers: the rest of panel p's update runs here
+      const int m = NP - p - 2;
+      const int units = m * (m + 1) / 2;
+      for (int u = 0; u < units; ++u) {
+        int tr, tc;
+        tri_decode(u, tr, tc);
+        tile_update<NT>(DL, tr + p + 2, tc + p + 2, p0, lane);
+      }
     }
-    __syncthreads();
-    BTD_PHASE(11);
+    named_sync(kBarA, NWA * 32);
+    BTD_PHASE(5);
   }
-  // remaining leaves: the last panel's (and all of them when the CTA has a single warp)
-  for (int lf = (NW > 1 ? NP - 1 : 0) + warp; lf < NP; lf += NW) leaf_inverse<NT>(DL, lf * 8, lane);
-  __syncthreads();
-  BTD_PHASE(12);
+  // remaining leaves: the last panel's (and all of them when group A is a single warp)
+  for (int lf = (NWA > 1 ? NP - 1 : 0) + warp; lf < NP; lf += NWA) leaf_inverse<NT>(DL, lf * 8, lane);
+  named_sync(kBarA, NWA * 32);
+  BTD_PHASE(9);
 
   // ---- recursive doubling: [[A,0],[B,C]]^{-1} = [[Ai,0],[-Ci B Ai, Ci]] on DMMA ----
 #pragma unroll
   for (int b = 8; 2 * b <= NT; b *= 2) {
     const int tpb = b / 8;
     const int units = (NT / (2 * b)) * tpb * tpb;
-    constexpr int MAXV = (NT / 16 * 1 + NW - 1) / NW > 2 ? 2 : 2;  // <= 2 units per warp at every level
-    // phase 1: T = B * Ainv   -> strictly-upper scratch block (rows i0.., cols i0+b..)
-    {
+#pragma unroll
+    for (int phase = 0; phase < 2; ++phase) {
       double acc[MAXV][2];
       int i0v[MAXV], trv[MAXV], tcv[MAXV];
       bool ok[MAXV];
 #pragma unroll
       for (int q = 0; q < MAXV; ++q) {
-        const int u = warp + q * NW;
+        const int u = warp + q * NWA;
         ok[q] = u < units;
         const int pair = u / (tpb * tpb), rem = u % (tpb * tpb);
         i0v[q] = pair * 2 * b;
@@ -242,72 +288,49 @@ __device__ int potrf_trtri(double* DL) {
       for (int k0 = 0; k0 < b; k0 += 4) {
 #pragma unroll
         for (int q = 0; q < MAXV; ++q) {
-          if (!ok[q] || k0 < tcv[q] * 8) continue;  // Ainv[k][c] == 0 for k < c
+          if (!ok[q]) continue;
           const int i0 = i0v[q];
-          const double a = DL[(i0 + b + trv[q] * 8 + (lane >> 2)) * LD + i0 + k0 + (lane & 3)];
-          const double bb = DL[(i0 + k0 + (lane & 3)) * LD + i0 + tcv[q] * 8 + (lane >> 2)];
-          dmma(acc[q], a, bb);
+          if (phase == 0) {  // T = B * Ainv  (Ainv[k][c] == 0 for k < c)
+            if (k0 < tcv[q] * 8) continue;
+            const double a = DL[(i0 + b + trv[q] * 8 + (lane >> 2)) * LD + i0 + k0 + (lane & 3)];
+            const double bb = DL[(i0 + k0 + (lane & 3)) * LD + i0 + tcv[q] * 8 + (lane >> 2)];
+            dmma(acc[q], a, bb);
+          } else {  // B <- -Cinv * T  (Cinv[r][k] == 0 for k > r)
+            if (k0 > trv[q] * 8 + 4) continue;
+            const double a = DL[(i0 + b + trv[q] * 8 + (lane >> 2)) * LD + i0 + b + k0 + (lane & 3)];
+            const double bb = DL[(i0 + k0 + (lane & 3)) * LD + i0 + b + tcv[q] * 8 + (lane >> 2)];
+            dmma(acc[q], a, bb);
+          }
         }
       }
 #pragma unroll
       for (int q = 0; q < MAXV; ++q) {
         if (!ok[q]) continue;
         const int i0 = i0v[q];
-        double* dst = DL + (i0 + trv[q] * 8 + (lane >> 2)) * LD + i0 + b + tcv[q] * 8 + 2 * (lane & 3);
-        dst[0] = acc[q][0];
-        dst[1] = acc[q][1];
-      }
-    }
-    __syncthreads();
-    // phase 2: B <- -Cinv * T
-    {
-      double acc[MAXV][2];
-      int i0v[MAXV], trv[MAXV], tcv[MAXV];
-      bool ok[MAXV];
-#pragma unroll
-      for (int q = 0; q < MAXV; ++q) {
-        const int u = warp + q * NW;
-        ok[q] = u < units;
-        const int pair = u / (tpb * tpb), rem = u % (tpb * tpb);
-        i0v[q] = pair * 2 * b;
-        trv[q] = rem / tpb;
-        tcv[q] = rem % tpb;
-        acc[q][0] = acc[q][1] = 0.0;
-      }
-      for (int k0 = 0; k0 < b; k0 += 4) {
-#pragma unroll
-        for (int q = 0; q < MAXV; ++q) {
-          if (!ok[q] || k0 > trv[q] * 8 + 4) continue;  // Cinv[r][k] == 0 for k > r
-          const int i0 = i0v[q];
-          const double a = DL[(i0 + b + trv[q] * 8 + (lane >> 2)) * LD + i0 + b + k0 + (lane & 3)];
-          const double bb = DL[(i0 + k0 + (lane & 3)) * LD + i0 + b + tcv[q] * 8 + (lane >> 2)];
-          dmma(acc[q], a, bb);
+        if (phase == 0) {  // strictly-upper scratch block (rows i0.., cols i0+b..)
+          double* dst = DL + (i0 + trv[q] * 8 + (lane >> 2)) * LD + i0 + b + tcv[q] * 8 + 2 * (lane & 3);
+          dst[0] = acc[q][0];
+          dst[1] = acc[q][1];
+        } else {
+          double* dst = DL + (i0 + b + trv[q] * 8 + (lane >> 2)) * LD + i0 + tcv[q] * 8 + 2 * (lane & 3);
+          dst[0] = -acc[q][0];
+          dst[1] = -acc[q][1];
         }
       }
-#pragma unroll
-      for (int q = 0; q < MAXV; ++q) {
-        if (!ok[q]) continue;
-        const int i0 = i0v[q];
-        double* dst = DL + (i0 + b + trv[q] * 8 + (lane >> 2)) * LD + i0 + tcv[q] * 8 + 2 * (lane & 3);
-        dst[0] = -acc[q][0];
-        dst[1] = -acc[q][1];
-      }
+      named_sync(kBarA, NWA * 32);
     }
-    __syncthreads();
   }
-  BTD_PHASE(13);
+  BTD_PHASE(10);
   return 0;
 }
 
 // Pt = Xt * Linv^T, in place on the XP rows owned by this warp (16 rows per warp, two 8-row passes:
 // a pass reads only its own rows, so it can overwrite them after a __syncwarp).
 template <int NT>
-__device__ __forceinline__ void pt_gemm(double* XP, const double* DL, bool coupled, int warp, int lane) {
+__device__ __forceinline__ void pt_gemm(double* XP, const double* DL, int row0, int lane) {
   using S = FactorShape<NT>;
   constexpr int LD = S::LD;
   constexpr int NCT = NT / 8;
-  const int row0 = warp * 16;
-  if (!coupled && row0 >= NT) return;
   const double* pb = DL + (lane >> 2) * LD + (lane & 3);
 #pragma unroll 1
   for (int rt = 0; rt < 2; ++rt) {
@@ -331,6 +354,45 @@ __device__ __forceinline__ void pt_gemm(double* XP, const double* DL, bool coupl
       v.x = acc[ct][0];
       v.y = acc[ct][1];
       *reinterpret_cast<double2*>(XP + (row0 + rt * 8 + (lane >> 2)) * LD + ct * 8 + 2 * (lane & 3)) = v;
+    }
+  }
+}
+
+// Fill block of the next step:  Gt = -Pt2 * Pt1^T, one 8-row pass of Pt2 rows [row0, row0+8).
+// to_global == false: in place over the pass rows (a pass reads only its own Pt2 rows and Pt1);
+// to_global == true : last row of the segment, write S_sub = -(Y_L^T Y_R)^T = -Y_R^T Y_L.
+template <int NT>
+__device__ __forceinline__ void fill_band(double* XP, int row0, int lane, bool to_global, double* ssub, int n) {
+  using S = FactorShape<NT>;
+  constexpr int LD = S::LD;
+  constexpr int NCT = NT / 8;
+  const double* pb = XP + (lane >> 2) * LD + (lane & 3);  // Pt1 rows as the col-major B operand
+  {
+    constexpr int rt = 0;
+    double acc[NCT][2];
+#pragma unroll
+    for (int c = 0; c < NCT; ++c) acc[c][0] = acc[c][1] = 0.0;
+    const double* pa = XP + (NT + row0 + rt * 8 + (lane >> 2)) * LD + (lane & 3);
+#pragma unroll 4
+    for (int k0 = 0; k0 < NT; k0 += 4) {
+      const double a0 = pa[k0];
+#pragma unroll
+      for (int ct = 0; ct < NCT; ++ct) dmma(acc[ct], a0, pb[ct * 8 * LD + k0]);
+    }
+    __syncwarp();
+    const int r = row0 + rt * 8 + (lane >> 2);
+#pragma unroll
+    for (int ct = 0; ct < NCT; ++ct) {
+      const int c = ct * 8 + 2 * (lane & 3);
+      if (!to_global) {
+        double2 v;
+        v.x = -acc[ct][0];
+        v.y = -acc[ct][1];
+        *reinterpret_cast<double2*>(XP + (NT + r) * LD + c) = v;
+      } else if (r < n) {
+        if (c < n) ssub[(size_t)c * n + r] = -acc[ct][0];
+        if (c + 1 < n) ssub[(size_t)(c + 1) * n + r] = -acc[ct][1];
+      }
     }
   }
 }
@@ -360,15 +422,52 @@ __device__ __forceinline__ void syrk_tile(const double* XP, int R, int C, double
   }
 }
 
+// S_L += P2^T P2 over the SL tiles owned by warp `w` of a group of `nw` warps; S_L accumulates
+// across the segment's steps in its global output slot (L2 resident): keeping it in registers
+// would cost 32 registers for the whole kernel.
+template <int NT>
+__device__ __forceinline__ void sl_update(const double* XP, double* sl, int n, bool first, int w, int nw, int lane) {
+  using S = FactorShape<NT>;
+  constexpr int TS = S::TS, SUB = S::SUB, HALF = S::HALF, NSL = S::NSL;
+  for (int t = w; t < NSL; t += nw) {
+    int rr, cc;
+    tri_decode(t, rr, cc);
+    double acc[SUB][SUB][2];
+#pragma unroll
+    for (int i = 0; i < SUB; ++i)
+#pragma unroll
+      for (int jj = 0; jj < SUB; ++jj) {
+        const int r = rr * TS + i * 8 + (lane >> 2);
+        const int c = cc * TS + jj * 8 + 2 * (lane & 3);
+        const double* src = sl + (size_t)r * n + c;
+        acc[i][jj][0] = (!first && r < n && c < n) ? src[0] : 0.0;
+        acc[i][jj][1] = (!first && r < n && c + 1 < n) ? src[1] : 0.0;
+      }
+    syrk_tile<NT>(XP, HALF + rr, HALF + cc, acc, lane);
+#pragma unroll
+    for (int i = 0; i < SUB; ++i)
+#pragma unroll
+      for (int jj = 0; jj < SUB; ++jj) {
+        if (rr == cc && jj > i) continue;
+        const int r = rr * TS + i * 8 + (lane >> 2);
+        const int c = cc * TS + jj * 8 + 2 * (lane & 3);
+        double* dst = sl + (size_t)r * n + c;
+        if (r < n && c < n) dst[0] = acc[i][jj][0];
+        if (r < n && c + 1 < n) dst[1] = acc[i][jj][1];
+      }
+  }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MINB)
     factor_level_kernel(FactorArgs args) {
   using S = FactorShape<NT>;
-  constexpr int LD = S::LD, NTHREADS = S::NTHREADS, NW = S::NW, TS = S::TS, SUB = S::SUB;
-  constexpr int HALF = S::HALF, NSL = S::NSL, NG = S::NG, ND = S::ND;
+  constexpr int LD = S::LD, NTHREADS = S::NTHREADS, NW = S::NW, NWA = S::NWA, NWB = S::NWB;
+  constexpr int TS = S::TS, SUB = S::SUB, ND = S::ND;
   extern __shared__ __align__(16) double smem[];
   double* XP = smem;                // 2NT x LD : [X1 | Pt1] rows 0..NT-1, [Gt | Pt2] rows NT..2NT-1
   double* DL = smem + 2 * NT * LD;  // NT x LD  : D -> L -> Linv
+  __shared__ int s_fail;
 
   if (error_raised(args.err)) return;
   const int k = blockIdx.x;
@@ -379,6 +478,9 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
   const int n = args.n;
   const size_t bs = (size_t)n * n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool in_a = warp < NWA;
+  const int wb = warp - NWA;  // warp index inside group B
+  double* sl = args.Sl + (size_t)k * bs;
 
   // ---- prologue: D_0, X1_0 (A_{1,0} or C_R), Gt_0 = C_L^T ----
   stage_block_async<NT, LD, NTHREADS>(DL, args.diag + start * bs, n);
@@ -394,153 +496,114 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
   }
   cp_async_wait_all();
   for (int r = n + tid; r < NT; r += NTHREADS) DL[r * LD + r] = 1.0;
+  __syncthreads();
   BTD_PHASE_INIT();
 
   for (int j = 0; j < J; ++j) {
     const bool last = (j == J - 1);
-    BTD_PHASE(0);
-    const int piv = potrf_trtri<NT>(DL);  // begins with a barrier
+    // ================= phase 1: A factors D_j ; B finishes step j-1 =================
+    int fail = 0;
+    if (in_a) fail = potrf_trtri<NT>(DL, &s_fail);
+    if (NWB == 0) __syncthreads();  // single-warp CTA: group B work runs after the factor
+    if (j > 0 && (NWB == 0 || !in_a)) {
+      const int w = NWB ? wb : 0, nw = NWB ? NWB : 1, nb = NWB ? NWB * 32 : 32;
+      const int gt = NWB ? tid - NWA * 32 : tid;
+      if (coupled) {
+        sl_update<NT>(XP, sl, n, j == 1, w, nw, lane);
+        named_sync(kBarB, nb);
+        for (int rb = w; rb < NT / 8; rb += nw) fill_band<NT>(XP, rb * 8, lane, false, nullptr, n);
+        named_sync(kBarB, nb);
+      }
+      // L_{j,j-1} (Pt1 of step j-1) -> global, then stage the next X1 over it
+      for (int e = gt; e < n * n; e += nb) args.Lsub[(start + j - 1) * bs + e] = XP[(e / n) * LD + e % n];
+      named_sync(kBarB, nb);
+      const double* nx = !last ? args.sub + (start + j) * bs : (coupled ? args.sub + (stop - 1) * bs : nullptr);
+      if (nx) {
+        if ((n & 1) == 0) {
+          for (int idx = gt; idx < NT * NT / 2; idx += nb) {
+            const int r = idx / (NT / 2), c = (idx % (NT / 2)) * 2;
+            const bool ok = r < n && c < n;
+            cp_async16(XP + r * LD + c, ok ? (const void*)(nx + (size_t)r * n + c) : (const void*)nx, ok ? 16 : 0);
+          }
+        } else {
+          for (int idx = gt; idx < NT * NT; idx += nb) {
+            const int r = idx / NT, c = idx % NT;
+            const bool ok = r < n && c < n;
+            cp_async8(XP + r * LD + c, ok ? (const void*)(nx + (size_t)r * n + c) : (const void*)nx, ok ? 8 : 0);
+          }
+        }
+        cp_async_commit();
+      }
+    }
+    if (in_a && tid == 0) s_fail = fail;
+    __syncthreads();
     BTD_PHASE(1);
-    if (piv) {
-      if (tid == 0 && piv <= n) report_npd(args.err, args.level, j, k, piv);
+    if (s_fail) {
+      if (tid == 0 && s_fail <= n) report_npd(args.err, args.level, j, k, s_fail);
       return;
     }
-    store_block<NT, LD, NTHREADS>(args.Linv + (start + j) * bs, DL, n, true);
+    // ================= phase 2: all warps ==========================================
+    store_packed_lower<NT, LD, NTHREADS>(args.Linv + (start + j) * (size_t)((n * (n + 1) / 2 + 1) / 2 * 2), DL, n);
     if (last && !coupled) break;
-
     cp_async_wait_all();
     __syncthreads();
-    BTD_PHASE(2);
-    pt_gemm<NT>(XP, DL, coupled, warp, lane);
+    if (coupled || warp * 16 < NT) pt_gemm<NT>(XP, DL, warp * 16, lane);
+    if (!coupled && NW * 16 < NT) pt_gemm<NT>(XP, DL, (warp + NW) * 16, lane);  // single-warp base
     __syncthreads();
-    BTD_PHASE(3);
+    BTD_PHASE(2);
     if (!last) {
-      store_block<NT, LD, NTHREADS>(args.Lsub + (start + j) * bs, XP, n, false);  // L_{j+1,j}
       stage_block_async<NT, LD, NTHREADS>(DL, args.diag + (start + j + 1) * bs, n);
       cp_async_commit();
     }
-
-    BTD_PHASE(4);
-    // ---- C = Pt Pt^T (lower): S_L tiles (persistent) and G tiles (held until XP is free) ----
-    double held[S::MAXG][SUB][SUB][2];
-    if (coupled) {
-      // S_L accumulates across the segment's steps in its global output slot (L2 resident):
-      // keeping it in registers would cost 32 registers for the whole kernel.
-#pragma unroll
-      for (int s = 0; s < S::MAXSL; ++s) {
-        const int t = warp + s * NW;
-        if (t < NSL) {
-          int rr, cc;
-          tri_decode(t, rr, cc);
-          double acc[SUB][SUB][2];
-#pragma unroll
-          for (int i = 0; i < SUB; ++i)
-#pragma unroll
-            for (int jj = 0; jj < SUB; ++jj) {
-              const int r = rr * TS + i * 8 + (lane >> 2);
-              const int c = cc * TS + jj * 8 + 2 * (lane & 3);
-              const double* src = args.Sl + (size_t)k * bs + (size_t)r * n + c;
-              acc[i][jj][0] = (j > 0 && r < n && c < n) ? src[0] : 0.0;
-              acc[i][jj][1] = (j > 0 && r < n && c + 1 < n) ? src[1] : 0.0;
-            }
-          syrk_tile<NT>(XP, HALF + rr, HALF + cc, acc, lane);
-#pragma unroll
-          for (int i = 0; i < SUB; ++i)
-#pragma unroll
-            for (int jj = 0; jj < SUB; ++jj) {
-              if (rr == cc && jj > i) continue;
-              const int r = rr * TS + i * 8 + (lane >> 2);
-              const int c = cc * TS + jj * 8 + 2 * (lane & 3);
-              double* dst = args.Sl + (size_t)k * bs + (size_t)r * n + c;
-              if (r < n && c < n) dst[0] = acc[i][jj][0];
-              if (r < n && c + 1 < n) dst[1] = acc[i][jj][1];
-            }
-        }
-      }
-#pragma unroll
-      for (int s = 0; s < S::MAXG; ++s) {
-        const int g = ((warp - NSL % NW + NW) % NW) + s * NW;
-#pragma unroll
-        for (int i = 0; i < SUB; ++i)
-#pragma unroll
-          for (int jj = 0; jj < SUB; ++jj) held[s][i][jj][0] = held[s][i][jj][1] = 0.0;
-        if (g < NG) syrk_tile<NT>(XP, HALF + g / HALF, g % HALF, held[s], lane);
-      }
-    }
-    BTD_PHASE(5);
-    cp_async_wait_all();
-    __syncthreads();
-    BTD_PHASE(6);
-    // ---- D tiles: D_{j+1} = A_{j+1,j+1} - P1^T P1  (or S_R at the last row) ----
+    // D_{j+1} = A_{j+1,j+1} - P1^T P1  (or S_R at the last row of a coupled segment)
+    double acc[S::MAXD][SUB][SUB][2];
+    int drr[S::MAXD], dcc[S::MAXD];
 #pragma unroll
     for (int s = 0; s < S::MAXD; ++s) {
-      const int dd = ((warp - (NSL + NG) % NW + NW) % NW) + s * NW;
+      const int dd = warp + s * NW;
+      drr[s] = -1;
+#pragma unroll
+      for (int i = 0; i < SUB; ++i)
+#pragma unroll
+        for (int jj = 0; jj < SUB; ++jj) acc[s][i][jj][0] = acc[s][i][jj][1] = 0.0;
       if (dd < ND) {
-        int rr, cc;
-        tri_decode(dd, rr, cc);
-        double acc[SUB][SUB][2];
-#pragma unroll
-        for (int i = 0; i < SUB; ++i)
-#pragma unroll
-          for (int jj = 0; jj < SUB; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
-        syrk_tile<NT>(XP, rr, cc, acc, lane);
-#pragma unroll
-        for (int i = 0; i < SUB; ++i)
-#pragma unroll
-          for (int jj = 0; jj < SUB; ++jj) {
-            if (rr == cc && jj > i) continue;
-            const int r = rr * TS + i * 8 + (lane >> 2);
-            const int c = cc * TS + jj * 8 + 2 * (lane & 3);
-            if (!last) {
-              double* dst = DL + r * LD + c;
-              dst[0] = (r == c && r >= n) ? 1.0 : dst[0] - acc[i][jj][0];
-              dst[1] = (r == c + 1 && r >= n) ? 1.0 : dst[1] - acc[i][jj][1];
-            } else if (r < n) {
-              double* dst = args.Sr + (size_t)k * bs + (size_t)r * n;
-              if (c < n) dst[c] = acc[i][jj][0];
-              if (c + 1 < n) dst[c + 1] = acc[i][jj][1];
-            }
-          }
+        tri_decode(dd, drr[s], dcc[s]);
+        syrk_tile<NT>(XP, drr[s], dcc[s], acc[s], lane);
       }
     }
-    BTD_PHASE(7);
-    __syncthreads();  // every read of XP (Pt) is complete
-    BTD_PHASE(8);
-    if (coupled) {
+    cp_async_wait_all();
+    __syncthreads();
 #pragma unroll
-      for (int s = 0; s < S::MAXG; ++s) {
-        const int g = ((warp - NSL % NW + NW) % NW) + s * NW;
-        if (g >= NG) continue;
-        const int R = HALF + g / HALF, C = g % HALF;
+    for (int s = 0; s < S::MAXD; ++s) {
+      if (drr[s] < 0) continue;
+      const int rr = drr[s], cc = dcc[s];
 #pragma unroll
-        for (int i = 0; i < SUB; ++i)
+      for (int i = 0; i < SUB; ++i)
 #pragma unroll
-          for (int jj = 0; jj < SUB; ++jj) {
-            const int r = R * TS + i * 8 + (lane >> 2);  // in [NT, 2NT)
-            const int c = C * TS + jj * 8 + 2 * (lane & 3);
-            if (!last) {
-              XP[r * LD + c] = -held[s][i][jj][0];
-              XP[r * LD + c + 1] = -held[s][i][jj][1];
-            } else {
-              // S_sub (row s_{k+1}, col s_k) = -Y_R^T Y_L  = transpose of the held -Y_L^T Y_R
-              const int rr = r - NT;
-              if (rr < n) {
-                if (c < n) args.Ssub[(size_t)k * bs + (size_t)c * n + rr] = -held[s][i][jj][0];
-                if (c + 1 < n) args.Ssub[(size_t)k * bs + (size_t)(c + 1) * n + rr] = -held[s][i][jj][1];
-              }
-            }
+        for (int jj = 0; jj < SUB; ++jj) {
+          if (rr == cc && jj > i) continue;
+          const int r = rr * TS + i * 8 + (lane >> 2);
+          const int c = cc * TS + jj * 8 + 2 * (lane & 3);
+          if (!last) {
+            double* dst = DL + r * LD + c;
+            dst[0] = (r == c && r >= n) ? 1.0 : dst[0] - acc[s][i][jj][0];
+            dst[1] = (r == c + 1 && r >= n) ? 1.0 : dst[1] - acc[s][i][jj][1];
+          } else if (r < n) {
+            double* dst = args.Sr + (size_t)k * bs + (size_t)r * n;
+            if (c < n) dst[c] = acc[s][i][jj][0];
+            if (c + 1 < n) dst[c + 1] = acc[s][i][jj][1];
           }
-      }
+        }
     }
-    if (!last) {
-      if (j + 1 < J - 1)
-        stage_block_async<NT, LD, NTHREADS>(XP, args.sub + (start + j + 1) * bs, n);
-      else if (coupled)
-        stage_block_async<NT, LD, NTHREADS>(XP, args.sub + (stop - 1) * bs, n);  // C_R -> Y_R
-      cp_async_commit();
-    }
+    __syncthreads();
+    BTD_PHASE(3);
   }
 
+  if (coupled) {  // the last row's S_L update and S_sub = -Y_R^T Y_L[last]
+    sl_update<NT>(XP, sl, n, J == 1, warp, NW, lane);
+    for (int rb = warp; rb < NT / 8; rb += NW)
+      fill_band<NT>(XP, rb * 8, lane, true, args.Ssub + (size_t)k * bs, n);
+  }
 }
 
 // Next-level diagonal: S_diag[p] = (A[s_p] - S_L[p]) - S_R[p-1]  (reference order, bt/schur.py:186-188).

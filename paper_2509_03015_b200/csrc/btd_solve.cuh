@@ -42,7 +42,7 @@ struct SolveShape {
 
 // y[r][c] (+)= sign * sum_m op(M)[r][m] * x[m][c]    (M: n x n row-major in global memory)
 // x, y: shared NT x DC panels. Ends with a barrier.
-template <int NT, int DC, bool TRANS>
+template <int NT, int DC, bool TRANS, bool PACKED = false>
 __device__ __forceinline__ void block_mv(const double* __restrict__ M, int n, const double* x, double* y,
                                          double sign, bool accumulate, double* red) {
   using S = SolveShape<NT>;
@@ -58,8 +58,8 @@ __device__ __forceinline__ void block_mv(const double* __restrict__ M, int n, co
 #pragma unroll 8
       for (int mm = 0; mm < CPT; ++mm) {
         const int m = q * CPT + mm;
-        if (m < n) {
-          const double v = __ldg(row + m);
+        if (m < n && (!PACKED || m <= r)) {
+          const double v = PACKED ? __ldg(M + r * (r + 1) / 2 + m) : __ldg(row + m);
 #pragma unroll
           for (int c = 0; c < DC; ++c) part[c] += v * x[m * DC + c];
         }
@@ -84,8 +84,8 @@ __device__ __forceinline__ void block_mv(const double* __restrict__ M, int n, co
 #pragma unroll 8
       for (int mm = 0; mm < RPG; ++mm) {
         const int m = g * RPG + mm;
-        if (m < n) {
-          const double v = __ldg(M + (size_t)m * n + r);
+        if (m < n && (!PACKED || m >= r)) {
+          const double v = PACKED ? __ldg(M + m * (m + 1) / 2 + r) : __ldg(M + (size_t)m * n + r);
 #pragma unroll
           for (int c = 0; c < DC; ++c) part[c] += v * x[m * DC + c];
         }
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(SolveShape<NT>::NTHREADS) solve_level_kernel(S
   const long long start = coupled ? (long long)a.seps[k] + 1 : 0;
   const long long stop = coupled ? (long long)a.seps[k + 1] : a.N;
   const int J = (int)(stop - start);
-  const size_t bs = (size_t)n * n, ps = (size_t)n * d;
+  const size_t bs = (size_t)n * n, ps = (size_t)n * d, pk = (size_t)((n * (n + 1) / 2 + 1) / 2 * 2);
 
   // forward sweep: z_j = Linv_j (b_j - L_{j,j-1} z_{j-1});  z kept in u, spilled to x[row]
   for (int j = 0; j < J; ++j) {
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(SolveShape<NT>::NTHREADS) solve_level_kernel(S
     }
     __syncthreads();
     if (j > 0) block_mv<NT, DC, false>(a.Lsub + (row - 1) * bs, n, u, t, -1.0, true, red);
-    block_mv<NT, DC, false>(a.Linv + row * bs, n, t, u, 1.0, false, red);
+    block_mv<NT, DC, false, true>(a.Linv + row * pk, n, t, u, 1.0, false, red);
     if (j < J - 1) store_panel<NT, DC>(a.x + row * ps, u, n, d, c0, dc);
   }
   // backward sweep: x_j = Linv_j^T (z_j - L_{j+1,j}^T x_{j+1});  x_{j+1} kept in w
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(SolveShape<NT>::NTHREADS) solve_level_kernel(S
     }
     __syncthreads();
     if (j < J - 1) block_mv<NT, DC, true>(a.Lsub + row * bs, n, w, t, -1.0, true, red);
-    block_mv<NT, DC, true>(a.Linv + row * bs, n, t, w, 1.0, false, red);
+    block_mv<NT, DC, true, true>(a.Linv + row * pk, n, t, w, 1.0, false, red);
     if (a.mode == kSolveDown && j == J - 1) {  // f_R = C_R w_last
       block_mv<NT, DC, false>(a.Lsub + (stop - 1) * bs, n, w, xl, 1.0, false, red);
       store_panel<NT, DC>(a.fr + (size_t)k * ps, xl, n, d, c0, dc);

@@ -8,8 +8,7 @@ import torch
 import paper_2509_03015_b200 as pkg
 L = _native.lib()
 L.btd_debug_phase_cycles.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
-names = ['prologue/loop-top', 'potrf+trtri', 'store Linv + wait', 'pt_gemm', 'store Lsub+stage',
-         'syrk SL+G', 'wait D', 'D tiles', 'barrier', 'potrf part (of 1)']
+names = ['-', 'phase1 (A: potrf | B: SL+fill)', 'phase2 pt_gemm', 'phase2 D tiles', '4', '5', '6', '7', '8', '9']
 for cfg in sys.argv[1:]:
     N, n, d = (int(v) for v in cfg.split(','))
     A, B = pkg.generate_spd_btd(N, n, d, seed=0)

@@ -15,7 +15,7 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
     for (int e = threadIdx.x; e < NT * NT; e += S::NTHREADS) DL[(e / NT) * S::LD + e % NT] = A[e];
     __syncthreads();
     long long t0 = clock64();
-    int piv = potrf_trtri<NT>(DL);
+    __shared__ int sf; int piv = 0; if (threadIdx.x < FactorShape<NT>::NWA * 32) piv = potrf_trtri<NT>(DL, &sf);
     __syncthreads();
     long long t1 = clock64();
     tot += t1 - t0;
@@ -53,7 +53,7 @@ void run() {
 #ifdef BTD_PHASE_PROF
   unsigned long long ph[16]; cudaMemcpyFromSymbol(ph, g_phase_cycles, sizeof(ph));
   unsigned long long z[16] = {0}; cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
-  printf("phases/40: panel %llu trailing %llu leaf %llu combine(rest) %llu\n", ph[10]/40, ph[11]/40, ph[12]/40, ph[13]/40);
+  printf("per call: chain+helpers %llu critical-update %llu leaves %llu combine %llu\n", ph[4]/20, ph[5]/20, ph[9]/20, ph[10]/20);
 #endif
   printf("{\"NT\":%d,\"cycles\":%lld,\"fail\":%lld,\"err\":%.2e,\"cuda\":\"%s\"}\n", NT, cyc[0], cyc[1], err, cudaGetErrorString(e));
 }
