@@ -163,26 +163,24 @@ cudaError_t dispatch_solve_dc(const btd::SolveArgs& a, unsigned grid_x, cudaStre
 
 template <int NT, int DC>
 cudaError_t launch_stream(const btd::SolveArgs& a, cudaStream_t s) {
-  using S = btd::Solve2Shape<NT>;
-  constexpr size_t smem = sizeof(double) * ((size_t)S::STAGES * (S::FULL + S::PACK + NT * DC) +
-                                            (size_t)(4 + S::ZMAX + S::PARTS) * NT * DC);
+  using T = btd::TmaShape<NT, DC>;
   static int blocks_per_sm = -1, sms = 0;
   if (blocks_per_sm < 0) {
-    cudaError_t e = cudaFuncSetAttribute(btd::solve_stream_kernel<NT, DC>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(btd::solve_tma_kernel<NT, DC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)T::SMEM);
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, btd::solve_stream_kernel<NT, DC>,
-                                                      S::NTHREADS, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, btd::solve_tma_kernel<NT, DC>, T::NTHREADS,
+                                                      T::SMEM);
     if (e != cudaSuccess) return e;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   const long long cap = (long long)blocks_per_sm * sms;
   const unsigned gx = (unsigned)(a.K < cap ? a.K : cap);
   dim3 grid(gx, (unsigned)((a.d + DC - 1) / DC));
-  btd::solve_stream_kernel<NT, DC><<<grid, S::NTHREADS, smem, s>>>(a);
+  btd::solve_tma_kernel<NT, DC><<<grid, T::NTHREADS, T::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -201,13 +199,6 @@ cudaError_t dispatch_stream(int nt, const btd::SolveArgs& a, cudaStream_t s) {
     case 64: return dispatch_stream_dc<64>(a, s);
   }
   return cudaErrorInvalidValue;
-}
-
-// longest interior segment of a level (the streaming solve caches z for segments up to ZMAX)
-int64_t max_segment(const LevelPlan& lp) {
-  int64_t m = 0;
-  for (int64_t k = 0; k < lp.K; ++k) m = std::max(m, lp.seps[k + 1] - lp.seps[k] - 1);
-  return m;
 }
 
 cudaError_t dispatch_solve(int nt, const btd::SolveArgs& a, unsigned grid_x, cudaStream_t s) {
@@ -569,7 +560,7 @@ int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, v
     a.K = (int)lp.K;
     a.mode = btd::kSolveDown;
     a.err = err;
-    e = h->nt >= 32 ? dispatch_stream(h->nt, a, stream) : dispatch_solve(h->nt, a, (unsigned)lp.K, stream);
+    e = (n == h->nt) ? dispatch_stream(h->nt, a, stream) : dispatch_solve(h->nt, a, (unsigned)lp.K, stream);
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(down)");
     btd::assemble_separator_rhs_kernel<<<(unsigned)lp.P, 128, 0, stream>>>(rhs_l[l], a.seps, rhs_l[l + 1], fr_l[l],
                                                                             (int)lp.K, n, (int)d, err);
@@ -588,7 +579,7 @@ int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, v
     a.K = 1;
     a.mode = btd::kSolveBase;
     a.err = err;
-    e = dispatch_solve(h->nt, a, 1u, stream);
+    e = (n == h->nt) ? dispatch_stream(h->nt, a, stream) : dispatch_solve(h->nt, a, 1u, stream);
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(base)");
   }
   for (size_t l = L; l-- > 0;) {
@@ -606,7 +597,7 @@ int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, v
     a.K = (int)lp.K;
     a.mode = btd::kSolveUp;
     a.err = err;
-    e = h->nt >= 32 ? dispatch_stream(h->nt, a, stream) : dispatch_solve(h->nt, a, (unsigned)lp.K, stream);
+    e = (n == h->nt) ? dispatch_stream(h->nt, a, stream) : dispatch_solve(h->nt, a, (unsigned)lp.K, stream);
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(up)");
   }
   return BTD_OK;

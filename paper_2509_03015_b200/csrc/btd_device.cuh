@@ -67,6 +67,39 @@ __device__ __forceinline__ void cp_async_wait_group() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// ---------------------------------------------------------------------------------------------
+// mbarrier + TMA 1D bulk copy (cp.async.bulk, SASS UBLKCP): one thread moves a whole contiguous
+// block global->shared; completion is tracked by transaction bytes on an mbarrier.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // Stage an n x n row-major global block into an NT x LD shared tile, zero-padding rows/cols >= n.
 template <int NT, int LD, int NTHREADS>
 __device__ __forceinline__ void stage_block_async(double* sm, const double* g, int n) {
@@ -130,19 +163,19 @@ __device__ __forceinline__ void store_block(double* g, const double* sm, int n, 
 }
 
 // Store the lower triangle of the n x n leading part of a shared tile in packed row-major form
-// (row r at offset r(r+1)/2): the inverse Cholesky factors are stored this way.
+// (row r at offset O_r, length L_r = 2 ceil((r+1)/2), zero padded; see packed_row_offset in
+// btd_solve2.cuh): the inverse Cholesky factors are stored this way.
+__host__ __device__ __forceinline__ int packed_offset_(int r) {
+  const int k = r >> 1;
+  return (r & 1) ? 2 * (k + 1) * (k + 1) : 2 * k * (k + 1);
+}
 template <int NT, int LD, int NTHREADS>
 __device__ __forceinline__ void store_packed_lower(double* g, const double* sm, int n) {
-  if (n == NT) {
-    for (int e = threadIdx.x; e < NT * NT; e += NTHREADS) {
-      const int r = e / NT, c = e % NT;
-      if (c <= r) g[r * (r + 1) / 2 + c] = sm[r * LD + c];
-    }
-  } else {
-    for (int e = threadIdx.x; e < n * n; e += NTHREADS) {
-      const int r = e / n, c = e % n;
-      if (c <= r) g[r * (r + 1) / 2 + c] = sm[r * LD + c];
-    }
+  // (r, c) for c <= r, plus the zero pad (r, r+1) of even rows
+  for (int e = threadIdx.x; e < n * (n + 1); e += NTHREADS) {
+    const int r = e / (n + 1), c = e % (n + 1);
+    const int len = ((r + 2) >> 1) << 1;
+    if (c < len) g[packed_offset_(r) + c] = (c <= r) ? sm[r * LD + c] : 0.0;
   }
 }
 

@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
       return;
     }
     // ================= phase 2: all warps ==========================================
-    store_packed_lower<NT, LD, NTHREADS>(args.Linv + (start + j) * (size_t)((n * (n + 1) / 2 + 1) / 2 * 2), DL, n);
+    store_packed_lower<NT, LD, NTHREADS>(args.Linv + (start + j) * (size_t)packed_offset_(n), DL, n);
     if (last && !coupled) break;
     cp_async_wait_all();
     __syncthreads();

@@ -59,7 +59,7 @@ __device__ __forceinline__ void block_mv(const double* __restrict__ M, int n, co
       for (int mm = 0; mm < CPT; ++mm) {
         const int m = q * CPT + mm;
         if (m < n && (!PACKED || m <= r)) {
-          const double v = PACKED ? __ldg(M + r * (r + 1) / 2 + m) : __ldg(row + m);
+          const double v = PACKED ? __ldg(M + packed_offset_(r) + m) : __ldg(row + m);
 #pragma unroll
           for (int c = 0; c < DC; ++c) part[c] += v * x[m * DC + c];
         }
@@ -85,7 +85,7 @@ __device__ __forceinline__ void block_mv(const double* __restrict__ M, int n, co
       for (int mm = 0; mm < RPG; ++mm) {
         const int m = g * RPG + mm;
         if (m < n && (!PACKED || m >= r)) {
-          const double v = PACKED ? __ldg(M + m * (m + 1) / 2 + r) : __ldg(M + (size_t)m * n + r);
+          const double v = PACKED ? __ldg(M + packed_offset_(m) + r) : __ldg(M + (size_t)m * n + r);
 #pragma unroll
           for (int c = 0; c < DC; ++c) part[c] += v * x[m * DC + c];
         }
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(SolveShape<NT>::NTHREADS) solve_level_kernel(S
   const long long start = coupled ? (long long)a.seps[k] + 1 : 0;
   const long long stop = coupled ? (long long)a.seps[k + 1] : a.N;
   const int J = (int)(stop - start);
-  const size_t bs = (size_t)n * n, ps = (size_t)n * d, pk = (size_t)((n * (n + 1) / 2 + 1) / 2 * 2);
+  const size_t bs = (size_t)n * n, ps = (size_t)n * d, pk = (size_t)packed_offset_(n);
 
   // forward sweep: z_j = Linv_j (b_j - L_{j,j-1} z_{j-1});  z kept in u, spilled to x[row]
   for (int j = 0; j < J; ++j) {
