@@ -1,0 +1,313 @@
+// Block sizes n > 64 (multiples of 64, e.g. BASELINE config 4 with n = 256): the same Y-form
+// recursion as btd_factor.cuh, sequenced on the host as a handful of batched launches per
+// elimination step.  Every launch is batched over the segments of a level (blockIdx.y = segment);
+// operand addresses are derived on the device from the level plan (separators, step j), so no
+// pointer arrays are built on the host.
+//
+//   big_potrf_kernel : one CTA per segment, blocked (64-tile) Cholesky + inverse of the n x n
+//                      diagonal block D_j (potrf_trtri<64> on diagonal tiles, DMMA tile GEMMs
+//                      for the panel solve, trailing update and the inverse)
+//   bt_gemm_kernel   : C = alpha op(A) op(B) + beta C_in on 64 x 64 output tiles (DMMA m8n8k4),
+//                      used for Pt = Xt Linv^T, the Schur/fill/diag updates and the solve panels
+//   bt_copy_kernel   : block copies / transposed copies (staging, coupling copies)
+#pragma once
+
+#include "btd_factor.cuh"
+
+namespace btd {
+
+constexpr int BT = 64;        // tile edge
+constexpr int BLD = BT + 4;   // shared tile leading dimension
+constexpr int BTHREADS = 256;
+
+// How a batch entry (segment k at step j) addresses an operand.
+enum OperandIndex : int {
+  kIdxSegRow = 0,   // block row seps[k] + 1 + j + delta of a level array (base: j + delta)
+  kIdxSeg = 1,      // per-segment workspace slot k (+ delta)
+  kIdxSegStop = 2,  // block row seps[k+1] + delta (the right separator side)
+  kIdxSegStart = 3  // block row seps[k] + delta (the left separator side)
+};
+
+struct Operand {
+  const double* base;
+  long long stride;  // doubles between consecutive indexed blocks
+  int ld;            // leading dimension (doubles) of the stored matrix
+  int index, delta;
+  int row0, col0;    // offset of the op()-matrix inside the stored block (before transposition)
+  int trans;         // op(X) = X^T
+};
+
+__device__ __forceinline__ const double* operand_ptr(const Operand& o, const int* seps, int base_mode, int k, int j) {
+  long long idx;
+  switch (o.index) {
+    case kIdxSegRow: idx = (base_mode ? 0ll : (long long)seps[k] + 1) + j + o.delta; break;
+    case kIdxSeg: idx = (long long)k + o.delta; break;
+    case kIdxSegStop: idx = (long long)seps[k + 1] + o.delta; break;
+    default: idx = (long long)seps[k] + o.delta; break;
+  }
+  return o.base + idx * o.stride;
+}
+
+// activity of a segment at step j
+enum Activity : int { kActAll = 0, kActNotLast = 1, kActLast = 2, kActBeforeSecondLast = 3, kActSecondLast = 4 };
+
+__device__ __forceinline__ bool segment_active(const int* seps, int base_mode, long long N, int k, int j, int act,
+                                               int& J) {
+  J = base_mode ? (int)N : seps[k + 1] - seps[k] - 1;
+  if (j >= J) return false;
+  if (act == kActNotLast) return j < J - 1;
+  if (act == kActLast) return j == J - 1;
+  if (act == kActBeforeSecondLast) return j < J - 2;
+  if (act == kActSecondLast) return j == J - 2;
+  return true;
+}
+
+struct GemmArgs {
+  Operand A, B, Cin, Cout;
+  const int* seps;
+  long long N;
+  int base_mode, j, act;
+  int m, n, k;           // op(A) m x k, op(B) k x n
+  double alpha, beta;    // Cout = alpha op(A) op(B) + beta Cin   (beta == 0: Cin unused)
+  int lower_only;        // skip tiles strictly above the diagonal (symmetric outputs)
+  int tri;               // 1: op(B)[k][c] == 0 for k > c (B = L^T, L lower); 2: op(A)[r][k] == 0 for k > r;
+                         // 3: op(A)[r][k] == 0 for k < r (A = L^T)
+  int store_trans;       // write Cout^T
+  int tiles_n;
+  const DevErr* err;
+};
+
+// Stage the 64 x 64 tile of op(X) at (r0, c0) (op-matrix coordinates, rows x cols bounded) into
+// shared memory S[r][c] (leading dimension BLD) with zero fill.
+__device__ __forceinline__ void stage_op_tile(double* S, const double* X, int ld, int trans, int r0, int c0,
+                                              int rows, int cols) {
+  for (int e = threadIdx.x; e < BT * BT; e += BTHREADS) {
+    int r, c;
+    if (!trans) {
+      r = e / BT, c = e % BT;  // coalesced along c
+    } else {
+      c = e / BT, r = e % BT;  // coalesced along r (stored row c0 + c)
+    }
+    const int gr = r0 + r, gc = c0 + c;
+    double* dst = S + r * BLD + c;
+    if (gr < rows && gc < cols) {
+      const double* src = trans ? X + (size_t)gc * ld + gr : X + (size_t)gr * ld + gc;
+      cp_async8(dst, src, 8);
+    } else {
+      *dst = 0.0;
+    }
+  }
+}
+
+// acc (warp tile 16 x 32) += As(64 x 64) * Bs(64 x 64)^T restricted to k in [k0, k1)
+__device__ __forceinline__ void tile_mma(double (&acc)[2][4][2], const double* As, const double* Bs, int k0, int k1) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rw = (warp >> 1) * 16, cw = (warp & 1) * 32;
+  const double* pa = As + (rw + (lane >> 2)) * BLD + (lane & 3);
+  const double* pb = Bs + (cw + (lane >> 2)) * BLD + (lane & 3);
+  for (int kk = k0; kk < k1; kk += 4) {
+    double a[2], b[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) a[i] = pa[i * 8 * BLD + kk];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) b[q] = pb[q * 8 * BLD + kk];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dmma(acc[i][q], a[i], b[q]);
+  }
+}
+
+// One 64 x 64 output tile at (m0, n0) of alpha op(A) op(B) (+ beta Cin): the k loop runs over
+// 64-wide chunks staged through two shared tiles (A chunk, B^T chunk).
+__device__ __forceinline__ void gemm_tile(double (&acc)[2][4][2], const double* A, int lda, int ta, const double* B,
+                                          int ldb, int tb, int m, int n, int kdim, int m0, int n0, int kbeg, int kend,
+                                          double* As, double* Bs) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[i][q][0] = acc[i][q][1] = 0.0;
+  for (int kc = kbeg; kc < kend; kc += BT) {
+    __syncthreads();
+    stage_op_tile(As, A, lda, ta, m0, kc, m, kdim);
+    // op(B) is kdim x n; we need Bs[c][k] = op(B)[kc + k][n0 + c] = op(B)^T tile
+    stage_op_tile(Bs, B, ldb, !tb, n0, kc, n, kdim);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    tile_mma(acc, As, Bs, 0, min(BT, kend - kc));
+  }
+}
+
+__global__ void __launch_bounds__(BTHREADS) bt_gemm_kernel(GemmArgs g) {
+  if (error_raised(g.err)) return;
+  const int k = blockIdx.y;
+  int J;
+  if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, g.act, J)) return;
+  const int tm = blockIdx.x / g.tiles_n, tn = blockIdx.x % g.tiles_n;
+  const int m0 = tm * BT, n0 = tn * BT;
+  if (g.lower_only && n0 > m0) return;
+  extern __shared__ __align__(16) double gsm[];
+  double* As = gsm;
+  double* Bs = gsm + BT * BLD;
+  const double* A = operand_ptr(g.A, g.seps, g.base_mode, k, g.j) + (size_t)g.A.row0 * g.A.ld + g.A.col0;
+  const double* B = operand_ptr(g.B, g.seps, g.base_mode, k, g.j) + (size_t)g.B.row0 * g.B.ld + g.B.col0;
+  int kbeg = 0, kend = g.k;
+  if (g.tri == 1) kend = min(kend, n0 + BT);
+  if (g.tri == 2) kend = min(kend, m0 + BT);
+  if (g.tri == 3) kbeg = m0 / BT * BT;
+  double acc[2][4][2];
+  gemm_tile(acc, A, g.A.ld, g.A.trans, B, g.B.ld, g.B.trans, g.m, g.n, g.k, m0, n0, kbeg, kend, As, Bs);
+  const double* Cin = g.beta != 0.0 ? operand_ptr(g.Cin, g.seps, g.base_mode, k, g.j) : nullptr;
+  if (Cin) Cin += (size_t)g.Cin.row0 * g.Cin.ld + g.Cin.col0;
+  double* Cout = const_cast<double*>(operand_ptr(g.Cout, g.seps, g.base_mode, k, g.j)) +
+                 (size_t)g.Cout.row0 * g.Cout.ld + g.Cout.col0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rw = (warp >> 1) * 16, cw = (warp & 1) * 32;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = m0 + rw + i * 8 + (lane >> 2);
+        const int c = n0 + cw + q * 8 + 2 * (lane & 3) + h;
+        if (r >= g.m || c >= g.n) continue;
+        double v = g.alpha * acc[i][q][h];
+        if (Cin) v += g.beta * Cin[(size_t)r * g.Cin.ld + c];
+        if (g.store_trans)
+          Cout[(size_t)c * g.Cout.ld + r] = v;
+        else
+          Cout[(size_t)r * g.Cout.ld + c] = v;
+      }
+}
+
+struct CopyArgs {
+  Operand src, dst;
+  const int* seps;
+  long long N;
+  int base_mode, j, act;
+  int rows, cols;  // of the destination
+  const DevErr* err;
+};
+
+// dst[r][c] = src[r][c] (or src[c][r] when src.trans); blockIdx.y = segment
+__global__ void bt_copy_kernel(CopyArgs c) {
+  if (error_raised(c.err)) return;
+  const int k = blockIdx.y;
+  int J;
+  if (!segment_active(c.seps, c.base_mode, c.N, k, c.j, c.act, J)) return;
+  const double* s = operand_ptr(c.src, c.seps, c.base_mode, k, c.j);
+  double* d = const_cast<double*>(operand_ptr(c.dst, c.seps, c.base_mode, k, c.j));
+  const long long tot = (long long)c.rows * c.cols;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / c.cols), col = (int)(e % c.cols);
+    const double v = c.src.trans ? s[(size_t)(c.src.row0 + col) * c.src.ld + c.src.col0 + r]
+                                 : s[(size_t)(c.src.row0 + r) * c.src.ld + c.src.col0 + col];
+    d[(size_t)(c.dst.row0 + r) * c.dst.ld + c.dst.col0 + col] = v;
+  }
+}
+
+struct BigPotrfArgs {
+  Operand D;     // n x n working block (in: D_j lower; out: L lower)
+  Operand Linv;  // n x n output (full, zero upper)
+  const int* seps;
+  long long N;
+  int base_mode, j, n, level;
+  DevErr* err;
+};
+
+// Blocked Cholesky + inverse of an n x n block (n = 64 NB), one CTA per segment.
+__global__ void __launch_bounds__(BTHREADS) big_potrf_kernel(BigPotrfArgs g) {
+  using S = FactorShape<64>;
+  constexpr int LD = S::LD;
+  if (error_raised(g.err)) return;
+  const int k = blockIdx.x;
+  int J;
+  if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, kActAll, J)) return;
+  extern __shared__ __align__(16) double sm[];
+  double* DL = sm;             // 64 x LD diagonal tile
+  double* As = DL + BT * LD;   // staging tiles for the tile GEMMs
+  double* Bs = As + BT * BLD;
+  __shared__ int s_fail;
+  double* D = const_cast<double*>(operand_ptr(g.D, g.seps, g.base_mode, k, g.j));
+  double* Li = const_cast<double*>(operand_ptr(g.Linv, g.seps, g.base_mode, k, g.j));
+  const int n = g.n, NB = n / BT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rw = (warp >> 1) * 16, cw = (warp & 1) * 32;
+  auto store_acc = [&](double* dst, int ld, double (&acc)[2][4][2], double sign, const double* addsrc) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = rw + i * 8 + (lane >> 2), c = cw + q * 8 + 2 * (lane & 3) + h;
+          const double v = sign * acc[i][q][h];
+          dst[(size_t)r * ld + c] = addsrc ? addsrc[(size_t)r * ld + c] + v : v;
+        }
+  };
+  double acc[2][4][2];
+  for (int kb = 0; kb < NB; ++kb) {
+    // diagonal tile -> DL, factor + invert (warps 0..3, named barrier 1)
+    __syncthreads();
+    for (int e = tid; e < BT * BT; e += BTHREADS) DL[(e / BT) * LD + e % BT] = D[(size_t)(kb * BT + e / BT) * n + kb * BT + e % BT];
+    __syncthreads();
+    int fail = 0;
+    if (warp < S::NWA) fail = potrf_trtri<64>(DL, &s_fail);
+    if (tid == 0) s_fail = fail;
+    __syncthreads();
+    if (s_fail) {
+      if (tid == 0) report_npd(g.err, g.level, g.j, k, kb * BT + s_fail);
+      return;
+    }
+    // Linv_kk -> Li (full tile, zero upper); L_kk is not needed again
+    for (int e = tid; e < BT * BT; e += BTHREADS) {
+      const int r = e / BT, c = e % BT;
+      Li[(size_t)(kb * BT + r) * n + kb * BT + c] = c <= r ? DL[r * LD + c] : 0.0;
+    }
+    // panel: L_ib = A_ib Linv_kk^T  (i > kb), in place in D
+    for (int ib = kb + 1; ib < NB; ++ib) {
+      gemm_tile(acc, D + (size_t)ib * BT * n + kb * BT, n, 0, Li + (size_t)kb * BT * n + kb * BT, n, 1, BT, BT, BT,
+                0, 0, 0, BT, As, Bs);
+      __syncthreads();
+      store_acc(D + (size_t)ib * BT * n + kb * BT, n, acc, 1.0, nullptr);
+    }
+    __syncthreads();
+    // trailing: A_ij -= L_ib L_jb^T  (kb < jb <= ib)
+    for (int ib = kb + 1; ib < NB; ++ib)
+      for (int jb = kb + 1; jb <= ib; ++jb) {
+        gemm_tile(acc, D + (size_t)ib * BT * n + kb * BT, n, 0, D + (size_t)jb * BT * n + kb * BT, n, 1, BT, BT, BT,
+                  0, 0, 0, BT, As, Bs);
+        __syncthreads();
+        double* t = D + (size_t)ib * BT * n + jb * BT;
+        store_acc(t, n, acc, -1.0, t);
+      }
+  }
+  __syncthreads();
+  // inverse, block row by block row: Linv_ij = -Linv_ii sum_{m=j}^{i-1} L_im Linv_mj  (i > j)
+  // T = sum_m L_im Linv_mj is formed in the (unused) strict upper tile D[j][i] as scratch.
+  for (int ib = 1; ib < NB; ++ib) {
+    for (int jb = 0; jb < ib; ++jb) {
+      // T = L[ib][jb..ib-1] * Linv[jb..ib-1][jb]   (k range (ib - jb) tiles)
+      gemm_tile(acc, D + (size_t)ib * BT * n + jb * BT, n, 0, Li + (size_t)jb * BT * n + jb * BT, n, 0, BT, BT,
+                (ib - jb) * BT, 0, 0, 0, (ib - jb) * BT, As, Bs);
+      __syncthreads();
+      store_acc(D + (size_t)jb * BT * n + ib * BT, n, acc, 1.0, nullptr);
+    }
+    __syncthreads();
+    for (int jb = 0; jb < ib; ++jb) {
+      gemm_tile(acc, Li + (size_t)ib * BT * n + ib * BT, n, 0, D + (size_t)jb * BT * n + ib * BT, n, 0, BT, BT, BT, 0,
+                0, 0, BT, As, Bs);
+      __syncthreads();
+      store_acc(Li + (size_t)ib * BT * n + jb * BT, n, acc, -1.0, nullptr);
+    }
+    __syncthreads();
+  }
+  // zero the strict upper off-diagonal tiles of Linv
+  for (int ib = 0; ib < NB; ++ib)
+    for (int jb = ib + 1; jb < NB; ++jb)
+      for (int e = tid; e < BT * BT; e += BTHREADS) Li[(size_t)(ib * BT + e / BT) * n + jb * BT + e % BT] = 0.0;
+}
+
+}  // namespace btd

@@ -14,6 +14,7 @@
 #include "btd_factor.cuh"
 #include "btd_solve.cuh"
 #include "btd_solve2.cuh"
+#include "btd_big.cuh"
 
 namespace {
 
@@ -41,6 +42,9 @@ struct btd_hierarchy {
   int64_t base_N = 0;
   bool overflow = false;
   size_t off_err = 0, off_base_linv = 0, off_base_lsub = 0;
+  bool big = false;              // n > 64: tiled path (btd_big.cuh), Linv stored full n x n
+  int64_t kmax = 1;              // most segments of any level (big-path workspaces)
+  size_t off_big_ws = 0;         // factor scratch: WD | WX | WP per segment
   size_t persistent_bytes = 0, scratch_bytes = 0;
   char* persistent = nullptr;
   bool factored = false;
@@ -246,6 +250,203 @@ int finish_check(btd_hierarchy* h, cudaStream_t stream, btd_status* st) {
   return BTD_OK;
 }
 
+
+// =============================================================================================
+// n > 64: host sequencing of the tiled path (btd_big.cuh)
+// =============================================================================================
+btd::Operand opnd(const double* base, long long stride, int ld, int index, int delta = 0, int row0 = 0,
+                  int trans = 0) {
+  btd::Operand o;
+  o.base = base;
+  o.stride = stride;
+  o.ld = ld;
+  o.index = index;
+  o.delta = delta;
+  o.row0 = row0;
+  o.col0 = 0;
+  o.trans = trans;
+  return o;
+}
+
+struct BigCtx {
+  const int* seps;
+  long long N;
+  int base_mode, K;
+  const btd::DevErr* err;
+  cudaStream_t s;
+};
+
+cudaError_t big_gemm(const BigCtx& c, int j, int act, btd::Operand A, btd::Operand B, btd::Operand Cin,
+                     btd::Operand Cout, int m, int n, int k, double alpha, double beta, int lower = 0, int tri = 0,
+                     int store_trans = 0) {
+  static bool configured = false;
+  const int smem = 2 * btd::BT * btd::BLD * (int)sizeof(double);
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(btd::bt_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  btd::GemmArgs g{};
+  g.A = A;
+  g.B = B;
+  g.Cin = Cin;
+  g.Cout = Cout;
+  g.seps = c.seps;
+  g.N = c.N;
+  g.base_mode = c.base_mode;
+  g.j = j;
+  g.act = act;
+  g.m = m;
+  g.n = n;
+  g.k = k;
+  g.alpha = alpha;
+  g.beta = beta;
+  g.lower_only = lower;
+  g.tri = tri;
+  g.store_trans = store_trans;
+  g.tiles_n = (n + btd::BT - 1) / btd::BT;
+  g.err = c.err;
+  dim3 grid((unsigned)(((m + btd::BT - 1) / btd::BT) * g.tiles_n), (unsigned)c.K);
+  btd::bt_gemm_kernel<<<grid, btd::BTHREADS, smem, c.s>>>(g);
+  return cudaGetLastError();
+}
+
+cudaError_t big_copy(const BigCtx& c, int j, int act, btd::Operand src, btd::Operand dst, int rows, int cols) {
+  btd::CopyArgs a{};
+  a.src = src;
+  a.dst = dst;
+  a.seps = c.seps;
+  a.N = c.N;
+  a.base_mode = c.base_mode;
+  a.j = j;
+  a.act = act;
+  a.rows = rows;
+  a.cols = cols;
+  a.err = c.err;
+  const long long tot = (long long)rows * cols;
+  dim3 grid((unsigned)std::min<long long>((tot + 255) / 256, 64), (unsigned)c.K);
+  btd::bt_copy_kernel<<<grid, 256, 0, c.s>>>(a);
+  return cudaGetLastError();
+}
+
+// One level (coupled) or the base (base_mode) of the tiled factorization.
+cudaError_t big_factor_level(const BigCtx& c, int level, int Jmax, int n, const double* diag, const double* sub,
+                             double* Linv, double* Lsub, double* Sl, double* Sr, double* Ssub, char* ws,
+                             btd::DevErr* err) {
+  using namespace btd;
+  const long long nn = (long long)n * n;
+  double* WD = (double*)ws;
+  double* WX = WD + (size_t)c.K * nn;
+  double* WP = WX + (size_t)c.K * 2 * nn;
+  const bool coupled = !c.base_mode;
+  const Operand oWD = opnd(WD, nn, n, kIdxSeg), oWX = opnd(WX, 2 * nn, n, kIdxSeg), oWP = opnd(WP, 2 * nn, n, kIdxSeg);
+  const Operand oWXhi = opnd(WX, 2 * nn, n, kIdxSeg, 0, n), oWPhi = opnd(WP, 2 * nn, n, kIdxSeg, 0, n);
+  const Operand oLinv = opnd(Linv, nn, n, kIdxSegRow);
+  cudaError_t e;
+#define BIG_CHECK(x)              \
+  do {                            \
+    e = (x);                      \
+    if (e != cudaSuccess) return e; \
+  } while (0)
+  // ---- prologue ----
+  BIG_CHECK(big_copy(c, 0, kActAll, opnd(diag, nn, n, kIdxSegRow), oWD, n, n));
+  if (coupled) {
+    BIG_CHECK(big_copy(c, 0, kActNotLast, opnd(sub, nn, n, kIdxSegRow), oWX, n, n));
+    BIG_CHECK(big_copy(c, 0, kActLast, opnd(sub, nn, n, kIdxSegStop, -1), oWX, n, n));
+    BIG_CHECK(big_copy(c, 0, kActAll, opnd(sub, nn, n, kIdxSegStart, 0, 0, 1), oWXhi, n, n));  // C_L^T
+    BIG_CHECK(big_copy(c, 0, kActAll, opnd(sub, nn, n, kIdxSegStart), opnd(Lsub, nn, n, kIdxSegStart), n, n));
+    BIG_CHECK(big_copy(c, 0, kActAll, opnd(sub, nn, n, kIdxSegStop, -1), opnd(Lsub, nn, n, kIdxSegStop, -1), n, n));
+  } else if (c.N > 1) {
+    BIG_CHECK(big_copy(c, 0, kActNotLast, opnd(sub, nn, n, kIdxSegRow), oWX, n, n));
+  }
+  for (int j = 0; j < Jmax; ++j) {
+    {
+      BigPotrfArgs a{};
+      a.D = oWD;
+      a.Linv = oLinv;
+      a.seps = c.seps;
+      a.N = c.N;
+      a.base_mode = c.base_mode;
+      a.j = j;
+      a.n = n;
+      a.level = level;
+      a.err = err;
+      const int smem = 3 * BT * FactorShape<64>::LD * (int)sizeof(double);
+      static bool conf = false;
+      if (!conf) {
+        BIG_CHECK(cudaFuncSetAttribute(big_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        conf = true;
+      }
+      big_potrf_kernel<<<(unsigned)c.K, BTHREADS, smem, c.s>>>(a);
+      BIG_CHECK(cudaGetLastError());
+    }
+    // Pt = Xt Linv^T
+    BIG_CHECK(big_gemm(c, j, coupled ? kActAll : kActNotLast, oWX, opnd(Linv, nn, n, kIdxSegRow, 0, 0, 1), oWP, oWP,
+                       coupled ? 2 * n : n, n, n, 1.0, 0.0, 0, 1));
+    if (coupled) {
+      // fill block G^T = -P2 P1^T, or at the last row S_sub = (-P2 P1^T)^T
+      const Operand oP1t = opnd(WP, 2 * nn, n, kIdxSeg, 0, 0, 1);
+      BIG_CHECK(big_gemm(c, j, kActNotLast, oWPhi, oP1t, oWXhi, oWXhi, n, n, n, -1.0, 0.0));
+      BIG_CHECK(big_gemm(c, j, kActLast, oWPhi, oP1t, opnd(Ssub, nn, n, kIdxSeg), opnd(Ssub, nn, n, kIdxSeg), n, n, n,
+                         -1.0, 0.0, 0, 0, 1));
+      // S_L (+)= P2 P2^T
+      const Operand oSl = opnd(Sl, nn, n, kIdxSeg);
+      BIG_CHECK(big_gemm(c, j, kActAll, oWPhi, opnd(WP, 2 * nn, n, kIdxSeg, 0, n, 1), oSl, oSl, n, n, n, 1.0,
+                         j > 0 ? 1.0 : 0.0, 1));
+      // S_R = P1 P1^T at the last row
+      BIG_CHECK(big_gemm(c, j, kActLast, oWP, oP1t, opnd(Sr, nn, n, kIdxSeg), opnd(Sr, nn, n, kIdxSeg), n, n, n, 1.0,
+                         0.0, 1));
+    }
+    // D_{j+1} = A_{j+1,j+1} - P1 P1^T ; L_{j+1,j} -> hierarchy ; next X1
+    BIG_CHECK(big_gemm(c, j, kActNotLast, oWP, opnd(WP, 2 * nn, n, kIdxSeg, 0, 0, 1), opnd(diag, nn, n, kIdxSegRow, 1),
+                       oWD, n, n, n, -1.0, 1.0, 1));
+    BIG_CHECK(big_copy(c, j, kActNotLast, oWP, opnd(Lsub, nn, n, kIdxSegRow), n, n));
+    BIG_CHECK(big_copy(c, j, kActBeforeSecondLast, opnd(sub, nn, n, kIdxSegRow, 1), oWX, n, n));
+    if (coupled) BIG_CHECK(big_copy(c, j, kActSecondLast, opnd(sub, nn, n, kIdxSegStop, -1), oWX, n, n));
+  }
+  return cudaSuccess;
+}
+
+// One level pass of the tiled solve.  mode: down (fold), up (boundary + solution), base.
+cudaError_t big_solve_level(const BigCtx& c, int mode, int Jmax, int n, int d, const double* rhs, const double* Linv,
+                            const double* Lsub, double* x, const double* xsep, double* fl, double* fr, double* Tws,
+                            double* Uws) {
+  using namespace btd;
+  const long long nn = (long long)n * n, ps = (long long)n * d;
+  const Operand oT = opnd(Tws, ps, d, kIdxSeg), oU = opnd(Uws, ps, d, kIdxSeg);
+  const Operand oX0 = opnd(x, ps, d, kIdxSegRow), oXm1 = opnd(x, ps, d, kIdxSegRow, -1), oXp1 = opnd(x, ps, d, kIdxSegRow, 1);
+  const Operand oR0 = opnd(rhs, ps, d, kIdxSegRow);
+  cudaError_t e;
+  // forward: z_j = Linv_j (b_j - L_{j,j-1} z_{j-1})
+  for (int j = 0; j < Jmax; ++j) {
+    if (j == 0)
+      BIG_CHECK(big_copy(c, 0, kActAll, oR0, oT, n, d));
+    else
+      BIG_CHECK(big_gemm(c, j, kActAll, opnd(Lsub, nn, n, kIdxSegRow, -1), oXm1, oR0, oT, n, d, n, -1.0, 1.0));
+    BIG_CHECK(big_gemm(c, j, kActAll, opnd(Linv, nn, n, kIdxSegRow), oT, oX0, oX0, n, d, n, 1.0, 0.0, 0, 2));
+  }
+  // backward: w_j = Linv_j^T (z_j - L_{j+1,j}^T w_{j+1})
+  const Operand oLinvT = opnd(Linv, nn, n, kIdxSegRow, 0, 0, 1);
+  for (int j = Jmax - 1; j >= 0; --j) {
+    // last row of the segment: w = Linv^T z
+    BIG_CHECK(big_gemm(c, j, kActLast, oLinvT, oX0, oU, oU, n, d, n, 1.0, 0.0, 0, 3));
+    if (mode != kSolveDown) BIG_CHECK(big_copy(c, j, kActLast, oU, oX0, n, d));
+    if (mode == kSolveDown)  // f_R = C_R w_last
+      BIG_CHECK(big_gemm(c, j, kActLast, opnd(Lsub, nn, n, kIdxSegStop, -1), oU, opnd(fr, ps, d, kIdxSeg),
+                         opnd(fr, ps, d, kIdxSeg), n, d, n, 1.0, 0.0));
+    // other rows: t = z_j - L_{j+1,j}^T w_{j+1} ; w_j = Linv_j^T t
+    const Operand oW1 = mode == kSolveDown ? oU : oXp1;
+    BIG_CHECK(big_gemm(c, j, kActNotLast, opnd(Lsub, nn, n, kIdxSegRow, 0, 0, 1), oW1, oX0, oT, n, d, n, -1.0, 1.0));
+    BIG_CHECK(big_gemm(c, j, kActNotLast, oLinvT, oT, mode == kSolveDown ? oU : oX0, mode == kSolveDown ? oU : oX0, n,
+                       d, n, 1.0, 0.0, 0, 3));
+  }
+  if (mode == kSolveDown)  // f_L = C_L^T w_0
+    BIG_CHECK(big_gemm(c, 0, kActAll, opnd(Lsub, nn, n, kIdxSegStart, 0, 0, 1), oU, opnd(fl, ps, d, kIdxSeg),
+                       opnd(fl, ps, d, kIdxSeg), n, d, n, 1.0, 0.0));
+  return cudaSuccess;
+#undef BIG_CHECK
+}
+
 }  // namespace
 
 extern "C" {
@@ -300,8 +501,10 @@ int btd_create(int64_t num_blocks, int64_t block_size, const btd_config* cfg, bt
     return BTD_ERR_UNSUPPORTED;
   }
   const int nt = pick_nt(block_size);
-  if (!nt) {
-    set_status(st, BTD_ERR_UNSUPPORTED, "block size %lld has no sm_100a kernel in this build (n <= 64)",
+  const bool big = !nt && block_size % 64 == 0 && block_size <= 1024;
+  if (!nt && !big) {
+    set_status(st, BTD_ERR_UNSUPPORTED,
+               "block size %lld has no sm_100a kernel in this build (n <= 64, or a multiple of 64 up to 1024)",
                (long long)block_size);
     return BTD_ERR_UNSUPPORTED;
   }
@@ -314,8 +517,9 @@ int btd_create(int64_t num_blocks, int64_t block_size, const btd_config* cfg, bt
   h->n = block_size;
   h->cfg = *cfg;
   h->nt = nt;
+  h->big = big;
   const size_t bb = (size_t)block_size * block_size * sizeof(double);
-  const size_t pb = (size_t)btd::packed_stride((int)block_size) * sizeof(double);
+  const size_t pb = big ? bb : (size_t)btd::packed_stride((int)block_size) * sizeof(double);
 
   // ---- recursion plan (recursive_factorize level loop, bt/schur.py:298-318) ----
   int64_t cur = num_blocks;
@@ -372,6 +576,11 @@ int btd_create(int64_t num_blocks, int64_t block_size, const btd_config* cfg, bt
     so = align_up(so + (size_t)(lp.P - 1) * bb);
     lp.off_sr = so;
     so = align_up(so + (size_t)lp.K * bb);
+    h->kmax = std::max<int64_t>(h->kmax, lp.K);
+  }
+  if (big) {
+    h->off_big_ws = so;
+    so = align_up(so + (size_t)h->kmax * 5 * bb);
   }
   h->scratch_bytes = std::max<size_t>(so, kAlign);
   *out = h;
@@ -436,6 +645,34 @@ int btd_factorize(btd_hierarchy* h, const double* diag, const double* sub, void*
 
   const double* cd = diag;
   const double* cs = sub;
+  if (h->big) {
+    for (size_t l = 0; l < h->levels.size(); ++l) {
+      LevelPlan& lp = h->levels[l];
+      int jmax = 0;
+      for (int64_t kk = 0; kk < lp.K; ++kk) jmax = std::max<int>(jmax, (int)(lp.seps[kk + 1] - lp.seps[kk] - 1));
+      BigCtx c{(const int*)(pers + lp.off_seps), lp.N, 0, (int)lp.K, err, stream};
+      double* next_diag = (double*)(scr + lp.off_next_diag);
+      e = big_factor_level(c, (int)l, jmax, n, cd, cs, (double*)(pers + lp.off_linv), (double*)(pers + lp.off_lsub),
+                           next_diag, (double*)(scr + lp.off_sr), (double*)(scr + lp.off_next_sub),
+                           scr + h->off_big_ws, err);
+      if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(big level)");
+      btd::assemble_schur_diag_kernel<<<(unsigned)lp.P, 256, 0, stream>>>(
+          cd, (const int*)(pers + lp.off_seps), next_diag, (const double*)(scr + lp.off_sr), (int)lp.K, n, err);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(assemble)");
+      cd = next_diag;
+      cs = (const double*)(scr + lp.off_next_sub);
+    }
+    if (!h->overflow) {
+      BigCtx c{nullptr, h->base_N, 1, 1, err, stream};
+      e = big_factor_level(c, (int)h->levels.size(), (int)h->base_N, n, cd, cs, (double*)(pers + h->off_base_linv),
+                           (double*)(pers + h->off_base_lsub), nullptr, nullptr, nullptr, scr + h->off_big_ws, err);
+      if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(big base)");
+    }
+    h->pending_check = true;
+    if (check) return finish_check(h, stream, st);
+    return BTD_OK;
+  }
   for (size_t l = 0; l < h->levels.size(); ++l) {
     LevelPlan& lp = h->levels[l];
     btd::FactorArgs a{};
@@ -504,6 +741,11 @@ int btd_solve_workspace(const btd_hierarchy* h, int64_t d, size_t* scratch_bytes
     so = align_up(so + (size_t)lp.P * pb);  // next x
     so = align_up(so + (size_t)lp.K * pb);  // f_R
   }
+  if (h->big) {  // T, U panels per segment and the boundary-modified rhs of a level
+    so = align_up(so + (size_t)h->kmax * pb);
+    so = align_up(so + (size_t)h->kmax * pb);
+    so = align_up(so + (size_t)h->N * pb);
+  }
   if (scratch_bytes) *scratch_bytes = std::max<size_t>(so, kAlign);
   return BTD_OK;
 }
@@ -544,6 +786,64 @@ int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, v
     so = align_up(so + (size_t)lp.K * pb);
   }
   cudaError_t e;
+  if (h->big) {
+    double* Tws = (double*)(scr + so);
+    so = align_up(so + (size_t)h->kmax * pb);
+    double* Uws = (double*)(scr + so);
+    so = align_up(so + (size_t)h->kmax * pb);
+    double* rmod = (double*)(scr + so);
+    const int dd = (int)d;
+    for (size_t l = 0; l < L; ++l) {
+      const LevelPlan& lp = h->levels[l];
+      int jmax = 0;
+      for (int64_t kk = 0; kk < lp.K; ++kk) jmax = std::max<int>(jmax, (int)(lp.seps[kk + 1] - lp.seps[kk] - 1));
+      const int* sp = (const int*)(pers + lp.off_seps);
+      BigCtx c{sp, lp.N, 0, (int)lp.K, err, stream};
+      e = big_solve_level(c, btd::kSolveDown, jmax, n, dd, rhs_l[l], (const double*)(pers + lp.off_linv),
+                          (const double*)(pers + lp.off_lsub), x_l[l], nullptr, rhs_l[l + 1], fr_l[l], Tws, Uws);
+      if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(big down)");
+      btd::assemble_separator_rhs_kernel<<<(unsigned)lp.P, 128, 0, stream>>>(rhs_l[l], sp, rhs_l[l + 1], fr_l[l],
+                                                                              (int)lp.K, n, dd, err);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(assemble)");
+    }
+    {
+      BigCtx c{nullptr, h->base_N, 1, 1, err, stream};
+      e = big_solve_level(c, btd::kSolveBase, (int)h->base_N, n, dd, rhs_l[L], (const double*)(pers + h->off_base_linv),
+                          (const double*)(pers + h->off_base_lsub), x_l[L], nullptr, nullptr, nullptr, Tws, Uws);
+      if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(big base)");
+    }
+    for (size_t l = L; l-- > 0;) {
+      const LevelPlan& lp = h->levels[l];
+      int jmax = 0;
+      for (int64_t kk = 0; kk < lp.K; ++kk) jmax = std::max<int>(jmax, (int)(lp.seps[kk + 1] - lp.seps[kk] - 1));
+      const int* sp = (const int*)(pers + lp.off_seps);
+      BigCtx c{sp, lp.N, 0, (int)lp.K, err, stream};
+      const long long nn = (long long)n * n, ps = (long long)n * dd;
+      const double* Ls = (const double*)(pers + lp.off_lsub);
+      // boundary-modified rhs: b_0 -= C_L x_L ; b_last -= C_R^T x_R
+      e = cudaMemcpyAsync(rmod, rhs_l[l], (size_t)lp.N * pb, cudaMemcpyDeviceToDevice, stream);
+      if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(big rmod)");
+      const btd::Operand rm0 = opnd(rmod, ps, dd, btd::kIdxSegRow), rmL = opnd(rmod, ps, dd, btd::kIdxSegStop, -1);
+      e = big_gemm(c, 0, btd::kActAll, opnd(Ls, nn, n, btd::kIdxSegStart), opnd(x_l[l + 1], ps, dd, btd::kIdxSeg), rm0,
+                   rm0, n, dd, n, -1.0, 1.0);
+      if (e == cudaSuccess)
+        e = big_gemm(c, 0, btd::kActAll, opnd(Ls, nn, n, btd::kIdxSegStop, -1, 0, 1),
+                     opnd(x_l[l + 1], ps, dd, btd::kIdxSeg, 1), rmL, rmL, n, dd, n, -1.0, 1.0);
+      if (e == cudaSuccess)
+        e = big_solve_level(c, btd::kSolveUp, jmax, n, dd, rmod, (const double*)(pers + lp.off_linv), Ls, x_l[l],
+                            x_l[l + 1], nullptr, nullptr, Tws, Uws);
+      // separator rows of the solution
+      if (e == cudaSuccess)
+        e = big_copy(c, 0, btd::kActAll, opnd(x_l[l + 1], ps, dd, btd::kIdxSeg), opnd(x_l[l], ps, dd, btd::kIdxSegStart),
+                     n, dd);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(x_l[l] + (size_t)lp.seps[lp.K] * ps, x_l[l + 1] + (size_t)lp.K * ps, (size_t)pb,
+                            cudaMemcpyDeviceToDevice, stream);
+      if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(big up)");
+    }
+    return BTD_OK;
+  }
   for (size_t l = 0; l < L; ++l) {
     const LevelPlan& lp = h->levels[l];
     btd::SolveArgs a{};

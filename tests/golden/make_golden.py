@@ -42,6 +42,8 @@ SOLVE_CASES = [
     (500, 6, 1, 11, 64, 8, True),
     (130, 24, 5, 12, 7, 6, False),
     (1024, 32, 1, 0, 64, 8, False),   # BASELINE config 1
+    (40, 128, 2, 13, 5, 3, False),     # n > 64 (tiled path)
+    (12, 192, 3, 14, 64, 8, False),    # n > 64, serial base only
 ]
 
 SCHUR_CASES = [  # level-0 Schur complement through the reference's own _factorize_level
@@ -59,6 +61,7 @@ NPD_CASES = [  # (N, n, seed, rho, crossover, negated global diag blocks)
     (40, 3, 0, 4, 4, (0,)),
     (20, 2, 1, 8, 64, (6,)),
     (300, 8, 2, 8, 64, (250, 251)),
+    (30, 128, 3, 4, 4, (7,)),
 ]
 
 GEN_CASES = [(1000, 8, 3, 0), (257, 5, 1, 7), (64, 64, 4, 1), (1, 3, 2, 5), (2, 1, 1, 9)]

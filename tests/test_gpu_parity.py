@@ -72,6 +72,7 @@ SWEEP = [  # (N, n, d, crossover, rho)
     (17, 1, 1, 2, 2), (33, 9, 2, 3, 3), (64, 16, 1, 64, 8), (65, 16, 1, 64, 8), (129, 17, 3, 8, 8),
     (200, 31, 2, 16, 5), (300, 33, 1, 64, 8), (111, 47, 4, 9, 4), (250, 63, 1, 64, 8),
     (260, 64, 3, 64, 8), (1000, 8, 1, 64, 8), (777, 12, 5, 10, 7), (90, 64, 6, 4, 2), (45, 6, 9, 3, 16),
+    (20, 128, 2, 4, 3), (70, 256, 3, 8, 8), (9, 192, 1, 2, 2), (3, 128, 65, 1, 1), (50, 256, 70, 64, 8),
 ]
 
 
@@ -123,8 +124,8 @@ def test_multi_column_equals_column_by_column():
         assert np.abs(xc[:, :, 0] - X[:, :, c]).max() <= 1e-13 * np.abs(X).max()
 
 
-@pytest.mark.parametrize("cfg", [(1024, 32, 1), (65536, 64, 1), (1048576, 8, 1)],
-                         ids=["cfg1", "cfg2", "cfg3"])
+@pytest.mark.parametrize("cfg", [(1024, 32, 1), (65536, 64, 1), (1048576, 8, 1), (4096, 256, 64)],
+                         ids=["cfg1", "cfg2", "cfg3", "cfg4"])
 def test_baseline_configs_residual(cfg):
     """Full BASELINE sizes: size-independent property (relative residual) + first rows vs oracle."""
     N, n, d = cfg
