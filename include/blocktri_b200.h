@@ -112,6 +112,26 @@ int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t num_
 int btd_level_factor(const btd_hierarchy* h, int64_t level, double* linv_out, double* lsub_out,
                      void* stream, btd_status* st);
 
+/* ---- Sharded (multi-GPU) building blocks, SURVEY.md §8e ----
+ * The global chain is cut at level-L separators into contiguous chunks [a_g, b_g] (shared boundary
+ * separators b_g = a_{g+1}); chunk g factors exactly `local_levels` levels of its own plan (which
+ * equals the global plan restricted to the chunk), never its two boundary separators.  The
+ * reduced system over the chunk's remaining separators (partial Schur diagonal at the two
+ * boundaries) is exported; the caller sums the boundary partials of neighbouring chunks (NCCL),
+ * factors the reduced global system with btd_factorize, and solves it between btd_solve_down
+ * (exports the chunk's reduced rhs partial) and btd_solve_up (imports the reduced solution).
+ * The boundary diagonal block / rhs panel must be given by exactly one side (the other passes 0). */
+int btd_create_partial(int64_t num_blocks, int64_t block_size, const btd_config* cfg, int64_t local_levels,
+                       btd_hierarchy** out, btd_status* st);
+int btd_reduced_size(const btd_hierarchy* h, int64_t* num_blocks);
+int btd_factorize_partial(btd_hierarchy* h, const double* diag, const double* sub, void* persistent, void* scratch,
+                          double* reduced_diag, double* reduced_sub, void* stream, int32_t check, btd_status* st);
+/* scratch (btd_solve_workspace) must be the same buffer for the down and up halves */
+int btd_solve_down(const btd_hierarchy* h, const double* rhs, double* x, int64_t num_columns, void* scratch,
+                   double* reduced_rhs_out, void* stream, btd_status* st);
+int btd_solve_up(const btd_hierarchy* h, const double* rhs, const double* reduced_x, double* x, int64_t num_columns,
+                 void* scratch, void* stream, btd_status* st);
+
 /* Optional per-launch timing: when enabled, btd_factorize records CUDA events on the caller's
  * stream around every factor kernel (one per level, then the base).  btd_kernel_times returns the
  * elapsed milliseconds of the last factorization's launches in that order. */

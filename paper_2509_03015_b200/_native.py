@@ -34,6 +34,7 @@ EXPORTED_SYMBOLS = (
     "btd_version", "btd_default_config", "btd_plan_separators", "btd_create", "btd_destroy",
     "btd_num_levels", "btd_level_info", "btd_factor_workspace", "btd_factorize", "btd_check",
     "btd_solve_workspace", "btd_solve", "btd_level_factor", "btd_profile_kernels", "btd_kernel_times",
+    "btd_create_partial", "btd_reduced_size", "btd_factorize_partial", "btd_solve_down", "btd_solve_up",
 )
 
 
@@ -97,6 +98,11 @@ def lib() -> ctypes.CDLL:
         L.btd_solve.argtypes = [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, P(BtdStatus)]
         L.btd_level_factor.argtypes = [c_vp, c_i64, c_vp, c_vp, c_vp, P(BtdStatus)]
         L.btd_profile_kernels.argtypes = [c_vp, c_i32]
+        L.btd_create_partial.argtypes = [c_i64, c_i64, P(BtdConfig), c_i64, P(c_vp), P(BtdStatus)]
+        L.btd_reduced_size.argtypes = [c_vp, P(c_i64)]
+        L.btd_factorize_partial.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, P(BtdStatus)]
+        L.btd_solve_down.argtypes = [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, P(BtdStatus)]
+        L.btd_solve_up.argtypes = [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, P(BtdStatus)]
         L.btd_kernel_times.argtypes = [c_vp, P(ctypes.c_float), c_i64, P(c_i64)]
         for name in EXPORTED_SYMBOLS:
             if name not in ("btd_version", "btd_default_config", "btd_destroy"):

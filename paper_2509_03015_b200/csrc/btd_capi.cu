@@ -43,6 +43,7 @@ struct btd_hierarchy {
   bool overflow = false;
   size_t off_err = 0, off_base_linv = 0, off_base_lsub = 0;
   bool big = false;              // n > 64: tiled path (btd_big.cuh), Linv stored full n x n
+  bool partial = false;          // sharded chunk: exactly `levels` local levels, no base
   int64_t kmax = 1;              // most segments of any level (big-path workspaces)
   size_t off_big_ws = 0;         // factor scratch: WD | WX | WP per segment
   size_t persistent_bytes = 0, scratch_bytes = 0;
@@ -59,6 +60,8 @@ struct btd_hierarchy {
 };
 
 namespace {
+
+enum SolvePhase : int { kPhaseFull = 0, kPhaseDown = 1, kPhaseUp = 2 };
 
 void prof_mark(btd_hierarchy* h, cudaStream_t s) {
   if (!h->profile) return;
@@ -447,6 +450,16 @@ cudaError_t big_solve_level(const BigCtx& c, int mode, int Jmax, int n, int d, c
 #undef BIG_CHECK
 }
 
+// reduced level-(L+1) system of a partial (sharded) hierarchy -> caller buffers
+cudaError_t export_reduced(const btd_hierarchy* h, const double* cd, const double* cs, double* red_diag,
+                           double* red_sub, cudaStream_t stream) {
+  const size_t bb = (size_t)h->n * h->n * sizeof(double);
+  cudaError_t e = cudaMemcpyAsync(red_diag, cd, (size_t)h->base_N * bb, cudaMemcpyDeviceToDevice, stream);
+  if (e == cudaSuccess && h->base_N > 1)
+    e = cudaMemcpyAsync(red_sub, cs, (size_t)(h->base_N - 1) * bb, cudaMemcpyDeviceToDevice, stream);
+  return e;
+}
+
 }  // namespace
 
 extern "C" {
@@ -480,7 +493,8 @@ int btd_plan_separators(int64_t num_blocks, const btd_config* cfg, int64_t* sepa
   return BTD_OK;
 }
 
-int btd_create(int64_t num_blocks, int64_t block_size, const btd_config* cfg, btd_hierarchy** out, btd_status* st) {
+static int create_impl(int64_t num_blocks, int64_t block_size, const btd_config* cfg, int64_t forced_levels,
+                       btd_hierarchy** out, btd_status* st) {
   clear_status(st);
   if (!out) {
     set_status(st, BTD_ERR_INVALID_ARGUMENT, "out is NULL");
@@ -523,11 +537,21 @@ int btd_create(int64_t num_blocks, int64_t block_size, const btd_config* cfg, bt
 
   // ---- recursion plan (recursive_factorize level loop, bt/schur.py:298-318) ----
   int64_t cur = num_blocks;
+  h->partial = forced_levels >= 0;
   while (true) {
-    if (!should_recurse(cur, *cfg)) break;
-    if ((int64_t)h->levels.size() >= cfg->max_levels) {
-      h->overflow = true;
-      break;
+    if (h->partial) {
+      if ((int64_t)h->levels.size() == forced_levels) break;
+      if (cur < 3) {
+        delete h;
+        set_status(st, BTD_ERR_INVALID_ARGUMENT, "chunk too short for %lld local levels", (long long)forced_levels);
+        return BTD_ERR_INVALID_ARGUMENT;
+      }
+    } else {
+      if (!should_recurse(cur, *cfg)) break;
+      if ((int64_t)h->levels.size() >= cfg->max_levels) {
+        h->overflow = true;
+        break;
+      }
     }
     LevelPlan lp;
     lp.N = cur;
@@ -559,7 +583,7 @@ int btd_create(int64_t num_blocks, int64_t block_size, const btd_config* cfg, bt
     lp.off_lsub = off;
     off = align_up(off + (size_t)(lp.N - 1) * bb);
   }
-  if (!h->overflow) {
+  if (!h->overflow && !h->partial) {
     h->off_base_linv = off;
     off = align_up(off + (size_t)h->base_N * pb);
     h->off_base_lsub = off;
@@ -585,6 +609,19 @@ int btd_create(int64_t num_blocks, int64_t block_size, const btd_config* cfg, bt
   h->scratch_bytes = std::max<size_t>(so, kAlign);
   *out = h;
   return BTD_OK;
+}
+
+int btd_create(int64_t num_blocks, int64_t block_size, const btd_config* cfg, btd_hierarchy** out, btd_status* st) {
+  return create_impl(num_blocks, block_size, cfg, -1, out, st);
+}
+
+int btd_create_partial(int64_t num_blocks, int64_t block_size, const btd_config* cfg, int64_t local_levels,
+                       btd_hierarchy** out, btd_status* st) {
+  if (local_levels < 1) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "local_levels must be >= 1");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  return create_impl(num_blocks, block_size, cfg, local_levels, out, st);
 }
 
 void btd_destroy(btd_hierarchy* h) { delete h; }
@@ -614,8 +651,8 @@ int btd_factor_workspace(const btd_hierarchy* h, size_t* persistent_bytes, size_
   return BTD_OK;
 }
 
-int btd_factorize(btd_hierarchy* h, const double* diag, const double* sub, void* persistent, void* scratch,
-                  void* stream_, int32_t check, btd_status* st) {
+static int factorize_impl(btd_hierarchy* h, const double* diag, const double* sub, void* persistent, void* scratch,
+                          void* stream_, int32_t check, btd_status* st, double* red_diag, double* red_sub) {
   clear_status(st);
   if (!h || !diag || !persistent || !scratch || (h->N > 1 && !sub)) {
     set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_factorize: NULL argument");
@@ -663,7 +700,10 @@ int btd_factorize(btd_hierarchy* h, const double* diag, const double* sub, void*
       cd = next_diag;
       cs = (const double*)(scr + lp.off_next_sub);
     }
-    if (!h->overflow) {
+    if (h->partial) {
+      e = export_reduced(h, cd, cs, red_diag, red_sub, stream);
+      if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize_partial(export)");
+    } else if (!h->overflow) {
       BigCtx c{nullptr, h->base_N, 1, 1, err, stream};
       e = big_factor_level(c, (int)h->levels.size(), (int)h->base_N, n, cd, cs, (double*)(pers + h->off_base_linv),
                            (double*)(pers + h->off_base_lsub), nullptr, nullptr, nullptr, scr + h->off_big_ws, err);
@@ -700,7 +740,10 @@ int btd_factorize(btd_hierarchy* h, const double* diag, const double* sub, void*
     cd = a.Sl;
     cs = a.Ssub;
   }
-  if (!h->overflow) {
+  if (h->partial) {
+    e = export_reduced(h, cd, cs, red_diag, red_sub, stream);
+    if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize_partial(export)");
+  } else if (!h->overflow) {
     btd::FactorArgs a{};
     a.diag = cd;
     a.sub = cs;
@@ -720,6 +763,30 @@ int btd_factorize(btd_hierarchy* h, const double* diag, const double* sub, void*
   }
   h->pending_check = true;
   if (check) return finish_check(h, stream, st);
+  return BTD_OK;
+}
+
+int btd_factorize(btd_hierarchy* h, const double* diag, const double* sub, void* persistent, void* scratch,
+                  void* stream, int32_t check, btd_status* st) {
+  if (h && h->partial) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "partial hierarchy: use btd_factorize_partial");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  return factorize_impl(h, diag, sub, persistent, scratch, stream, check, st, nullptr, nullptr);
+}
+
+int btd_factorize_partial(btd_hierarchy* h, const double* diag, const double* sub, void* persistent, void* scratch,
+                          double* reduced_diag, double* reduced_sub, void* stream, int32_t check, btd_status* st) {
+  if (!h || !h->partial || !reduced_diag || !reduced_sub) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_factorize_partial needs a partial hierarchy and output buffers");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  return factorize_impl(h, diag, sub, persistent, scratch, stream, check, st, reduced_diag, reduced_sub);
+}
+
+int btd_reduced_size(const btd_hierarchy* h, int64_t* num_blocks) {
+  if (!h || !num_blocks) return BTD_ERR_INVALID_ARGUMENT;
+  *num_blocks = h->base_N;
   return BTD_OK;
 }
 
@@ -750,8 +817,8 @@ int btd_solve_workspace(const btd_hierarchy* h, int64_t d, size_t* scratch_bytes
   return BTD_OK;
 }
 
-int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, void* scratch, void* stream_,
-              btd_status* st) {
+static int solve_impl(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, void* scratch, void* stream_,
+                      btd_status* st, int phase, const double* red_in, double* red_out) {
   clear_status(st);
   if (!h || !rhs || !x || !scratch || d < 1) {
     set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_solve: NULL argument or d < 1");
@@ -793,7 +860,7 @@ int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, v
     so = align_up(so + (size_t)h->kmax * pb);
     double* rmod = (double*)(scr + so);
     const int dd = (int)d;
-    for (size_t l = 0; l < L; ++l) {
+    for (size_t l = 0; l < L && phase != kPhaseUp; ++l) {
       const LevelPlan& lp = h->levels[l];
       int jmax = 0;
       for (int64_t kk = 0; kk < lp.K; ++kk) jmax = std::max<int>(jmax, (int)(lp.seps[kk + 1] - lp.seps[kk] - 1));
@@ -807,7 +874,14 @@ int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, v
       e = cudaGetLastError();
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(assemble)");
     }
-    {
+    if (phase == kPhaseDown) {
+      e = cudaMemcpyAsync(red_out, rhs_l[L], (size_t)h->base_N * pb, cudaMemcpyDeviceToDevice, stream);
+      return e == cudaSuccess ? BTD_OK : cuda_fail(st, e, "btd_solve_down(export)");
+    }
+    if (phase == kPhaseUp) {
+      e = cudaMemcpyAsync(x_l[L], red_in, (size_t)h->base_N * pb, cudaMemcpyDeviceToDevice, stream);
+      if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve_up(import)");
+    } else {
       BigCtx c{nullptr, h->base_N, 1, 1, err, stream};
       e = big_solve_level(c, btd::kSolveBase, (int)h->base_N, n, dd, rhs_l[L], (const double*)(pers + h->off_base_linv),
                           (const double*)(pers + h->off_base_lsub), x_l[L], nullptr, nullptr, nullptr, Tws, Uws);
@@ -844,7 +918,7 @@ int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, v
     }
     return BTD_OK;
   }
-  for (size_t l = 0; l < L; ++l) {
+  for (size_t l = 0; l < L && phase != kPhaseUp; ++l) {
     const LevelPlan& lp = h->levels[l];
     btd::SolveArgs a{};
     a.rhs = rhs_l[l];
@@ -867,7 +941,14 @@ int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, v
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(assemble)");
   }
-  {
+  if (phase == kPhaseDown) {
+    e = cudaMemcpyAsync(red_out, rhs_l[L], (size_t)h->base_N * pb, cudaMemcpyDeviceToDevice, stream);
+    return e == cudaSuccess ? BTD_OK : cuda_fail(st, e, "btd_solve_down(export)");
+  }
+  if (phase == kPhaseUp) {
+    e = cudaMemcpyAsync(x_l[L], red_in, (size_t)h->base_N * pb, cudaMemcpyDeviceToDevice, stream);
+    if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve_up(import)");
+  } else {
     btd::SolveArgs a{};
     a.rhs = rhs_l[L];
     a.Linv = (const double*)(pers + h->off_base_linv);
@@ -901,6 +982,33 @@ int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, v
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(up)");
   }
   return BTD_OK;
+}
+
+int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, void* scratch, void* stream,
+              btd_status* st) {
+  if (h && h->partial) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "partial hierarchy: use btd_solve_down / btd_solve_up");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  return solve_impl(h, rhs, x, d, scratch, stream, st, kPhaseFull, nullptr, nullptr);
+}
+
+int btd_solve_down(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, void* scratch,
+                   double* reduced_rhs_out, void* stream, btd_status* st) {
+  if (!h || !h->partial || !reduced_rhs_out) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_solve_down needs a partial hierarchy and an output buffer");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  return solve_impl(h, rhs, x, d, scratch, stream, st, kPhaseDown, nullptr, reduced_rhs_out);
+}
+
+int btd_solve_up(const btd_hierarchy* h, const double* rhs, const double* reduced_x, double* x, int64_t d,
+                 void* scratch, void* stream, btd_status* st) {
+  if (!h || !h->partial || !reduced_x) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_solve_up needs a partial hierarchy and the reduced solution");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  return solve_impl(h, rhs, x, d, scratch, stream, st, kPhaseUp, reduced_x, nullptr);
 }
 
 int btd_level_factor(const btd_hierarchy* h, int64_t level, double* linv_out, double* lsub_out, void* stream,
