@@ -13,8 +13,8 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libblocktri_b200.so")
-_SOURCES = [os.path.join(_HERE, "csrc", f) for f in
-            ("btd_capi.cu", "btd_factor.cuh", "btd_solve.cuh", "btd_device.cuh")] + \
+_SOURCES = sorted(os.path.join(_HERE, "csrc", f) for f in os.listdir(os.path.join(_HERE, "csrc"))
+                  if f.endswith((".cu", ".cuh"))) + \
            [os.path.join(os.path.dirname(_HERE), "include", "blocktri_b200.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
