@@ -137,6 +137,8 @@ int btd_solve_up(const btd_hierarchy* h, const double* rhs, const double* reduce
  * elapsed milliseconds of the last factorization's launches in that order. */
 int btd_profile_kernels(btd_hierarchy* h, int32_t enable);
 int btd_kernel_times(const btd_hierarchy* h, float* ms_out, int64_t cap, int64_t* count);
+/* Process-wide count of kernels this library has launched (evidence for bench.py gpu_launches). */
+long long btd_launch_count(void);
 
 #ifdef __cplusplus
 }

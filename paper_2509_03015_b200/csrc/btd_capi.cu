@@ -3,20 +3,26 @@
 #include "../../include/blocktri_b200.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
 #include <vector>
 
 #include "btd_factor.cuh"
+#include "btd_factor2.cuh"
 #include "btd_solve.cuh"
 #include "btd_solve2.cuh"
 #include "btd_big.cuh"
 
 namespace {
+
+// every kernel this library launches (btd_launch_count: bench.py gpu_launches)
+std::atomic<long long> g_launches{0};
 
 constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
@@ -140,11 +146,36 @@ cudaError_t launch_factor(const btd::FactorArgs& a, unsigned grid, cudaStream_t 
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  btd::factor_level_kernel<NT><<<grid, S::NTHREADS, S::SMEM, s>>>(a);
+  btd::factor_level_kernel<NT><<<grid, S::NTHREADS, S::SMEM, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+// Paired-segment schedule (btd_factor2.cuh) for a coupled level at NT = 64: experimental, off
+// unless BTD_PAIR=1 (it measured slower than two independent CTAs per SM).
+bool use_pair(int nt, const btd::FactorArgs& a) {
+  static int env = -1;
+  if (env < 0) {
+    const char* v = getenv("BTD_PAIR");
+    env = (v && v[0] == '1') ? 1 : 0;
+  }
+  return env && nt == 64 && !a.base && a.K >= 2;
+}
+
+cudaError_t launch_pair64(const btd::FactorArgs& a, cudaStream_t s) {
+  using P = btd::PairShape<64>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(btd::factor_pair_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)P::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  btd::factor_pair_kernel<64><<<(unsigned)((a.K + 1) / 2), P::NTHREADS, P::SMEM, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
 cudaError_t dispatch_factor(int nt, const btd::FactorArgs& a, unsigned grid, cudaStream_t s) {
+  if (use_pair(nt, a)) return launch_pair64(a, s);
   switch (nt) {
     case 8: return launch_factor<8>(a, grid, s);
     case 16: return launch_factor<16>(a, grid, s);
@@ -157,7 +188,7 @@ cudaError_t dispatch_factor(int nt, const btd::FactorArgs& a, unsigned grid, cud
 template <int NT, int DC>
 cudaError_t launch_solve(const btd::SolveArgs& a, unsigned grid_x, cudaStream_t s) {
   dim3 grid(grid_x, (unsigned)((a.d + DC - 1) / DC));
-  btd::solve_level_kernel<NT, DC><<<grid, btd::SolveShape<NT>::NTHREADS, 0, s>>>(a);
+  btd::solve_level_kernel<NT, DC><<<grid, btd::SolveShape<NT>::NTHREADS, 0, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
@@ -187,7 +218,7 @@ cudaError_t launch_stream(const btd::SolveArgs& a, cudaStream_t s) {
   const long long cap = (long long)blocks_per_sm * sms;
   const unsigned gx = (unsigned)(a.K < cap ? a.K : cap);
   dim3 grid(gx, (unsigned)((a.d + DC - 1) / DC));
-  btd::solve_tma_kernel<NT, DC><<<grid, T::NTHREADS, T::SMEM, s>>>(a);
+  btd::solve_tma_kernel<NT, DC><<<grid, T::NTHREADS, T::SMEM, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
@@ -310,7 +341,7 @@ cudaError_t big_gemm(const BigCtx& c, int j, int act, btd::Operand A, btd::Opera
   g.tiles_n = (n + btd::BT - 1) / btd::BT;
   g.err = c.err;
   dim3 grid((unsigned)(((m + btd::BT - 1) / btd::BT) * g.tiles_n), (unsigned)c.K);
-  btd::bt_gemm_kernel<<<grid, btd::BTHREADS, smem, c.s>>>(g);
+  btd::bt_gemm_kernel<<<grid, btd::BTHREADS, smem, c.s>>>(g); g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
@@ -328,7 +359,7 @@ cudaError_t big_copy(const BigCtx& c, int j, int act, btd::Operand src, btd::Ope
   a.err = c.err;
   const long long tot = (long long)rows * cols;
   dim3 grid((unsigned)std::min<long long>((tot + 255) / 256, 64), (unsigned)c.K);
-  btd::bt_copy_kernel<<<grid, 256, 0, c.s>>>(a);
+  btd::bt_copy_kernel<<<grid, 256, 0, c.s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
@@ -380,7 +411,7 @@ cudaError_t big_factor_level(const BigCtx& c, int level, int Jmax, int n, const 
         BIG_CHECK(cudaFuncSetAttribute(big_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         conf = true;
       }
-      big_potrf_kernel<<<(unsigned)c.K, BTHREADS, smem, c.s>>>(a);
+      big_potrf_kernel<<<(unsigned)c.K, BTHREADS, smem, c.s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
       BIG_CHECK(cudaGetLastError());
     }
     // Pt = Xt Linv^T
@@ -665,7 +696,7 @@ static int factorize_impl(btd_hierarchy* h, const double* diag, const double* su
   h->factored = false;
   const int n = (int)h->n;
   btd::DevErr* err = (btd::DevErr*)(pers + h->off_err);
-  btd::init_err_kernel<<<1, 1, 0, stream>>>(err);
+  btd::init_err_kernel<<<1, 1, 0, stream>>>(err); g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(init)");
 
@@ -674,7 +705,7 @@ static int factorize_impl(btd_hierarchy* h, const double* diag, const double* su
   for (auto& lp : h->levels) {
     const unsigned blocks = (unsigned)((lp.P + 255) / 256);
     btd::fill_separators_kernel<<<blocks, 256, 0, stream>>>((int*)(pers + lp.off_seps), (int)lp.P, (int)lp.N,
-                                                            (int)(h->cfg.segment_length + 1));
+                                                            (int)(h->cfg.segment_length + 1)); g_launches.fetch_add(1, std::memory_order_relaxed);
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(seps)");
@@ -689,12 +720,14 @@ static int factorize_impl(btd_hierarchy* h, const double* diag, const double* su
       for (int64_t kk = 0; kk < lp.K; ++kk) jmax = std::max<int>(jmax, (int)(lp.seps[kk + 1] - lp.seps[kk] - 1));
       BigCtx c{(const int*)(pers + lp.off_seps), lp.N, 0, (int)lp.K, err, stream};
       double* next_diag = (double*)(scr + lp.off_next_diag);
+      prof_mark(h, stream);
       e = big_factor_level(c, (int)l, jmax, n, cd, cs, (double*)(pers + lp.off_linv), (double*)(pers + lp.off_lsub),
                            next_diag, (double*)(scr + lp.off_sr), (double*)(scr + lp.off_next_sub),
                            scr + h->off_big_ws, err);
+      prof_mark(h, stream);
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(big level)");
       btd::assemble_schur_diag_kernel<<<(unsigned)lp.P, 256, 0, stream>>>(
-          cd, (const int*)(pers + lp.off_seps), next_diag, (const double*)(scr + lp.off_sr), (int)lp.K, n, err);
+          cd, (const int*)(pers + lp.off_seps), next_diag, (const double*)(scr + lp.off_sr), (int)lp.K, n, err); g_launches.fetch_add(1, std::memory_order_relaxed);
       e = cudaGetLastError();
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(assemble)");
       cd = next_diag;
@@ -705,8 +738,10 @@ static int factorize_impl(btd_hierarchy* h, const double* diag, const double* su
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize_partial(export)");
     } else if (!h->overflow) {
       BigCtx c{nullptr, h->base_N, 1, 1, err, stream};
+      prof_mark(h, stream);
       e = big_factor_level(c, (int)h->levels.size(), (int)h->base_N, n, cd, cs, (double*)(pers + h->off_base_linv),
                            (double*)(pers + h->off_base_lsub), nullptr, nullptr, nullptr, scr + h->off_big_ws, err);
+      prof_mark(h, stream);
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(big base)");
     }
     h->pending_check = true;
@@ -734,7 +769,7 @@ static int factorize_impl(btd_hierarchy* h, const double* diag, const double* su
     e = dispatch_factor(h->nt, a, (unsigned)lp.K, stream);
     prof_mark(h, stream);
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(level kernel)");
-    btd::assemble_schur_diag_kernel<<<(unsigned)lp.P, 256, 0, stream>>>(cd, a.seps, a.Sl, a.Sr, (int)lp.K, n, err);
+    btd::assemble_schur_diag_kernel<<<(unsigned)lp.P, 256, 0, stream>>>(cd, a.seps, a.Sl, a.Sr, (int)lp.K, n, err); g_launches.fetch_add(1, std::memory_order_relaxed);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(assemble)");
     cd = a.Sl;
@@ -870,7 +905,7 @@ static int solve_impl(const btd_hierarchy* h, const double* rhs, double* x, int6
                           (const double*)(pers + lp.off_lsub), x_l[l], nullptr, rhs_l[l + 1], fr_l[l], Tws, Uws);
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(big down)");
       btd::assemble_separator_rhs_kernel<<<(unsigned)lp.P, 128, 0, stream>>>(rhs_l[l], sp, rhs_l[l + 1], fr_l[l],
-                                                                              (int)lp.K, n, dd, err);
+                                                                              (int)lp.K, n, dd, err); g_launches.fetch_add(1, std::memory_order_relaxed);
       e = cudaGetLastError();
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(assemble)");
     }
@@ -937,7 +972,7 @@ static int solve_impl(const btd_hierarchy* h, const double* rhs, double* x, int6
     e = (n == h->nt) ? dispatch_stream(h->nt, a, stream) : dispatch_solve(h->nt, a, (unsigned)lp.K, stream);
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(down)");
     btd::assemble_separator_rhs_kernel<<<(unsigned)lp.P, 128, 0, stream>>>(rhs_l[l], a.seps, rhs_l[l + 1], fr_l[l],
-                                                                            (int)lp.K, n, (int)d, err);
+                                                                            (int)lp.K, n, (int)d, err); g_launches.fetch_add(1, std::memory_order_relaxed);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(assemble)");
   }
@@ -1069,5 +1104,7 @@ int btd_kernel_times(const btd_hierarchy* h, float* ms_out, int64_t cap, int64_t
   }
   return BTD_OK;
 }
+
+long long btd_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 }  // extern "C"

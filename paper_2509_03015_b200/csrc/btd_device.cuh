@@ -39,6 +39,21 @@ __device__ __forceinline__ bool error_raised(const DevErr* e) {
   return *((volatile const unsigned long long*)&e->key) != kNoErr;
 }
 
+// A factor kernel of level `level` may skip its remaining work only when the error already recorded
+// can no longer be superseded: it comes from an earlier level, or from an earlier (step, member) of
+// this level than the step `j` this segment would run next (the reference reports the earliest
+// step, then the lowest member).  Skipping on any error would lose an earlier failure of a CTA that
+// starts after another CTA of the same level failed.
+__device__ __forceinline__ bool npd_superseded(const DevErr* e, int level, long long j, long long member) {
+  const unsigned long long key = *((volatile const unsigned long long*)&e->key);
+  if (key == kNoErr) return false;
+  const int lvl = *((volatile const int*)&e->level);
+  if (lvl < level) return true;
+  const long long jerr = (long long)(key >> 43);
+  const long long merr = (long long)((key >> 16) & ((1ull << 27) - 1));
+  return j > jerr || (j == jerr && member > merr);
+}
+
 // ---------------------------------------------------------------------------------------------
 // fp64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col).
 // Fragment ownership (lane l): a = A[l/4][l%4], b = B[l%4][l/4], d = {D[l/4][2(l%4)], D[l/4][2(l%4)+1]}.

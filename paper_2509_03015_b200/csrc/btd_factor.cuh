@@ -82,6 +82,10 @@ struct FactorShape {
   static_assert(NWB == 0 || 16 * NWB == NT, "group B owns 16 rows of the fill block per warp");
 };
 
+#ifndef BTD_RCP_CHAIN
+#define BTD_RCP_CHAIN true
+#endif
+
 constexpr int kBarA = 1;  // named barrier of group A
 constexpr int kBarB = 2;  // named barrier of group B
 
@@ -130,13 +134,37 @@ __device__ __forceinline__ void leaf_inverse(double* DL, int d0, int lane) {
   }
 }
 
+// fp64 reciprocal / reciprocal square root for the pivot chain: the MUFU seed (rcp.approx: 27
+// cycles, rsqrt.approx: 74 cycles measured, tools/fp64_mix.cu) refined by two Newton steps, instead
+// of the libdevice sequences (rsqrt(double) ~75 + special-case handling, 1.0/x ~80 cycles).
+// Inputs are positive normal pivots (a non-positive pivot is reported, its values discarded).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const double h = x * r;
+    const double e = fma(-h, r, 1.0);  // 1 - x r^2
+    r = fma(0.5 * r, e, r);
+  }
+  return r;
+}
+
 // One 8-column panel of the Cholesky factorization, factored by a single warp in registers
 // (lane l owns panel rows p0+l and, when HASB, p0+l+32).  The pivot chain is latency bound
 // (shfl -> rsqrt -> fma per column); it is software-pipelined so that the next column's pivot and
 // multipliers are shuffled right after that column's own update, ahead of the other updates.
 // Branch-free: a data-dependent `break` costs ~40% of the chain (tools/panel_bench.cu); a failed
 // pivot only poisons values that are discarded.  Returns the 1-based failing pivot or 0.
-template <int NT, bool HASB>
+template <int NT, bool HASB, bool RCP = false>
 __device__ __forceinline__ int panel_chain(double* DL, int p0, int lane) {
   constexpr int LD = FactorShape<NT>::LD;
   const int ra = p0 + lane, rb = p0 + lane + 32;
@@ -161,8 +189,14 @@ __device__ __forceinline__ int panel_chain(double* DL, int p0, int lane) {
       if (HASB) u[c] = vb[kk] * lck[c];
     }
     fail = (fail == 0 && d <= 0.0) ? p0 + kk + 1 : fail;
-    const double rinv = rsqrt(d);
-    const double dinv = rinv * rinv;
+    double rinv, dinv;
+    if (RCP) {  // 1/d on the chain (rcp seed + Newton), the root off it
+      dinv = rcp_nr(d);
+      rinv = rsqrt_nr(d);
+    } else {
+      rinv = rsqrt(d);
+      dinv = rinv * rinv;
+    }
     double nd = 0.0, nl[8];
     if (kk + 1 < 8) {
       va[kk + 1] = fma(-t[kk + 1], dinv, va[kk + 1]);
@@ -205,6 +239,43 @@ __device__ __forceinline__ void tile_update(double* DL, int tr, int tc, int p0, 
   dst[1] -= acc[1];
 }
 
+// Rank-8 updates by the panel at column p0 of the lower-triangular tile set
+// {(off + tr, off + tc) : 0 <= tc <= tr < m}, units u = first, first + step, ...  Processed in
+// batches of B tiles with every fragment load issued before the DMMAs (ILP: one tile's
+// LDS -> DMMA -> DMMA -> LDS/STS chain is ~150 cycles).
+template <int NT, int B>
+__device__ __forceinline__ void tile_update_tri(double* DL, int off, int m, int first, int step, int p0, int lane) {
+  constexpr int LD = FactorShape<NT>::LD;
+  const int units = m * (m + 1) / 2;
+  for (int u0 = first; u0 < units; u0 += B * step) {
+    double a0[B], a1[B], b0[B], b1[B];
+    int tr[B], tc[B];
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const int u = u0 + q * step;
+      tri_decode(u < units ? u : 0, tr[q], tc[q]);
+      tr[q] += off;
+      tc[q] += off;
+      const double* pa = DL + (tr[q] * 8 + (lane >> 2)) * LD + p0 + (lane & 3);
+      const double* pb = DL + (tc[q] * 8 + (lane >> 2)) * LD + p0 + (lane & 3);
+      a0[q] = pa[0];
+      a1[q] = pa[4];
+      b0[q] = pb[0];
+      b1[q] = pb[4];
+    }
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      if (u0 + q * step >= units) continue;
+      double acc[2] = {0.0, 0.0};
+      dmma(acc, a0[q], b0[q]);
+      dmma(acc, a1[q], b1[q]);
+      double* dst = DL + (tr[q] * 8 + (lane >> 2)) * LD + tc[q] * 8 + 2 * (lane & 3);
+      dst[0] -= acc[0];
+      dst[1] -= acc[1];
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // In-place Cholesky + triangular inverse of the NT x NT tile DL (lower triangle is read), run by
 // the NWA warps of group A (named barrier kBarA).  Returns the 1-based first non-positive pivot
@@ -212,11 +283,13 @@ __device__ __forceinline__ void tile_update(double* DL, int tr, int tc, int p0, 
 // LAPACK/OpenBLAS path, so NaN propagates silently), or 0 -- uniform over group A.
 //
 // Panel-blocked right-looking Cholesky with look-ahead: warp 0 factors panel p (panel_chain)
-// while the other warps of the group apply panel p-1's update to the column blocks >= p+1 and
-// invert panel p-1's 8x8 diagonal tile (trtri leaf).  Only the update of column block p+1 by
-// panel p sits between two pivot chains.  The inverse is finished by recursive doubling on DMMA.
+// while the other warps of the group apply panel p-1's update to the column blocks >= p+1
+// (batched DMMA tiles) and invert panel p-1's 8x8 diagonal tile (trtri leaf).  Only the update of
+// column block p+1 by panel p sits between two pivot chains.
+// INVERSE = true : the full inverse is finished by recursive doubling on DMMA (DL -> Linv).
+// INVERSE = false: DL holds L with its 8x8 diagonal tiles replaced by their inverses.
 // ------------------------------------------------------------------------------------------
-template <int NT>
+template <int NT, bool INVERSE = true>
 __device__ int potrf_trtri(double* DL, int* s_fail) {
   using S = FactorShape<NT>;
   constexpr int LD = S::LD;
@@ -229,18 +302,13 @@ __device__ int potrf_trtri(double* DL, int* s_fail) {
   for (int p = 0; p < NP; ++p) {
     const int p0 = p * 8;
     if (warp == 0) {
-      const int f = (p0 + 32 < NT) ? panel_chain<NT, true>(DL, p0, lane) : panel_chain<NT, false>(DL, p0, lane);
+      const int f = (p0 + 32 < NT) ? panel_chain<NT, true, BTD_RCP_CHAIN>(DL, p0, lane)
+                                   : panel_chain<NT, false, BTD_RCP_CHAIN>(DL, p0, lane);
       if (lane == 0) *s_fail = f;
     } else if (p > 0) {
       // helpers: leaf of panel p-1, and panel p-1's update of the column blocks >= p+1
       if (warp == 1 + (p - 1) % (NWA > 1 ? NWA - 1 : 1)) leaf_inverse<NT>(DL, p0 - 8, lane);
-      const int m = NP - p - 1;  // column blocks p+1 .. NP-1
-      const int units = m * (m + 1) / 2;
-      for (int u = warp - 1; u < units; u += NWA - 1) {
-        int tr, tc;
-        tri_decode(u, tr, tc);
-        tile_update<NT>(DL, tr + p + 1, tc + p + 1, p0 - 8, lane);
-      }
+      tile_update_tri<NT, 4>(DL, p + 1, NP - p - 1, warp - 1, NWA - 1, p0 - 8, lane);
     }
     named_sync(kBarA, NWA * 32);
     BTD_PHASE(4);
@@ -248,15 +316,8 @@ __device__ int potrf_trtri(double* DL, int* s_fail) {
     if (fail) return fail;
     // critical: panel p's update of column block p+1 (tiles (tr, p+1), tr >= p+1)
     for (int tr = p + 1 + warp; tr < NP; tr += NWA) tile_update<NT>(DL, tr, p + 1, p0, lane);
-    if (NWA == 1) {  // no helpers: the rest of panel p's update runs here
-      const int m = NP - p - 2;
-      const int units = m * (m + 1) / 2;
-      for (int u = 0; u < units; ++u) {
-        int tr, tc;
-        tri_decode(u, tr, tc);
-        tile_update<NT>(DL, tr + p + 2, tc + p + 2, p0, lane);
-      }
-    }
+    if (NWA == 1 && p + 2 < NP)  // no helpers: the rest of panel p's update runs here
+      tile_update_tri<NT, 4>(DL, p + 2, NP - p - 2, 0, 1, p0, lane);
     named_sync(kBarA, NWA * 32);
     BTD_PHASE(5);
   }
@@ -264,6 +325,7 @@ __device__ int potrf_trtri(double* DL, int* s_fail) {
   for (int lf = (NWA > 1 ? NP - 1 : 0) + warp; lf < NP; lf += NWA) leaf_inverse<NT>(DL, lf * 8, lane);
   named_sync(kBarA, NWA * 32);
   BTD_PHASE(9);
+  if (!INVERSE) return 0;
 
   // ---- recursive doubling: [[A,0],[B,C]]^{-1} = [[Ai,0],[-Ci B Ai, Ci]] on DMMA ----
 #pragma unroll
@@ -469,7 +531,7 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
   double* DL = smem + 2 * NT * LD;  // NT x LD  : D -> L -> Linv
   __shared__ int s_fail;
 
-  if (error_raised(args.err)) return;
+  if (npd_superseded(args.err, args.level, 0, blockIdx.x)) return;
   const int k = blockIdx.x;
   const bool coupled = !args.base;
   const long long start = coupled ? (long long)args.seps[k] + 1 : 0;

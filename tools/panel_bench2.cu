@@ -1,9 +1,10 @@
-// panel_chain<NT,HASB> from btd_factor.cuh timed in isolation (one warp), vs context effects.
+// panel_chain (shuffle chain) vs panel_chain_fast (redundant diagonal tile) from btd_factor.cuh,
+// timed in isolation (one warp, one CTA).
 #include <cstdio>
 #include "../paper_2509_03015_b200/csrc/btd_factor.cuh"
 using namespace btd;
-template <int NT, bool HB>
-__global__ void k(const double* A, double* out, long long* cyc, int reps, int slot) {
+template <int NT, int V>
+__global__ void k(const double* A, double* out, long long* cyc, int reps, int slot, int p0) {
   constexpr int LD = FactorShape<NT>::LD;
   __shared__ double DL[NT * LD];
   long long tot = 0;
@@ -12,7 +13,8 @@ __global__ void k(const double* A, double* out, long long* cyc, int reps, int sl
     for (int e = threadIdx.x; e < NT * NT; e += 32) DL[(e / NT) * LD + e % NT] = A[e];
     __syncwarp();
     long long t0 = clock64();
-    f += panel_chain<NT, HB>(DL, 0, threadIdx.x);
+    if (V == 0) f += panel_chain<NT, true, false>(DL, p0, threadIdx.x);
+    else f += panel_chain<NT, true, true>(DL, p0, threadIdx.x);
     __syncwarp();
     long long t1 = clock64();
     tot += t1 - t0;
@@ -26,10 +28,11 @@ int main() {
   double *A, *o; long long* c; cudaMalloc(&A, sizeof(h)); cudaMalloc(&o, 8192); cudaMallocManaged(&c, 128);
   cudaMemcpy(A, h, sizeof(h), cudaMemcpyHostToDevice);
   for (int it = 0; it < 2; ++it) {
-    k<64, true><<<1, 32>>>(A, o, c, 50, 0);
-    k<64, false><<<1, 32>>>(A, o, c, 50, 1);
-    k<8, false><<<1, 32>>>(A, o, c, 50, 2);
+    k<64, 0><<<1, 32>>>(A, o, c, 50, 0, 0);
+    k<64, 1><<<1, 32>>>(A, o, c, 50, 1, 0);
+    k<64, 0><<<1, 32>>>(A, o, c, 50, 2, 48);
+    k<64, 1><<<1, 32>>>(A, o, c, 50, 3, 48);
     cudaDeviceSynchronize();
   }
-  printf("{\"chain64_hasb\":%lld,\"chain64_nob\":%lld,\"chain8\":%lld}\n", c[0], c[1], c[2]);
+  printf("{\"old_p0\":%lld,\"fast_p0\":%lld,\"old_p6\":%lld,\"fast_p6\":%lld}\n", c[0], c[1], c[2], c[3]);
 }
