@@ -14,7 +14,7 @@
 #include <vector>
 
 #include "btd_factor.cuh"
-#include "btd_factor2.cuh"
+#include "btd_factor3.cuh"
 #include "btd_solve.cuh"
 #include "btd_solve2.cuh"
 #include "btd_big.cuh"
@@ -150,32 +150,43 @@ cudaError_t launch_factor(const btd::FactorArgs& a, unsigned grid, cudaStream_t 
   return cudaGetLastError();
 }
 
-// Paired-segment schedule (btd_factor2.cuh) for a coupled level at NT = 64: experimental, off
-// unless BTD_PAIR=1 (it measured slower than two independent CTAs per SM).
-bool use_pair(int nt, const btd::FactorArgs& a) {
-  static int env = -1;
-  if (env < 0) {
-    const char* v = getenv("BTD_PAIR");
-    env = (v && v[0] == '1') ? 1 : 0;
+// Streaming schedule (btd_factor3.cuh) at NT = 64 for levels that fit in one wave of one CTA per
+// SM (and the base): its per-step latency is lower than factor_level_kernel's, but with one CTA
+// per SM it sustains less DMMA throughput on wide levels (measured: level 0 of cfg2 9.1 ms vs
+// 6.6 ms), where two factor_level_kernel CTAs per SM hide each other's pivot chains better.
+// BTD_STREAM=0 / 1 forces it off / on everywhere (A/B timing).
+bool use_stream(int nt, const btd::FactorArgs& a) {
+  static int env = -2;
+  if (env == -2) {
+    const char* v = getenv("BTD_STREAM");
+    env = !v ? -1 : (v[0] == '0' ? 0 : 1);
   }
-  return env && nt == 64 && !a.base && a.K >= 2;
+  if (nt != 64 || env == 0) return false;
+  if (env == 1) return true;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return a.base || a.K <= sms;
 }
 
-cudaError_t launch_pair64(const btd::FactorArgs& a, cudaStream_t s) {
-  using P = btd::PairShape<64>;
+cudaError_t launch_stream64(const btd::FactorArgs& a, unsigned grid, cudaStream_t s) {
+  using SS = btd::StreamShape;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(btd::factor_pair_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)P::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(btd::factor_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SS::SMEM);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  btd::factor_pair_kernel<64><<<(unsigned)((a.K + 1) / 2), P::NTHREADS, P::SMEM, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
+  btd::factor_stream_kernel<<<grid, SS::NTHREADS, SS::SMEM, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
 cudaError_t dispatch_factor(int nt, const btd::FactorArgs& a, unsigned grid, cudaStream_t s) {
-  if (use_pair(nt, a)) return launch_pair64(a, s);
+  if (use_stream(nt, a)) return launch_stream64(a, grid, s);
   switch (nt) {
     case 8: return launch_factor<8>(a, grid, s);
     case 16: return launch_factor<16>(a, grid, s);

@@ -290,7 +290,7 @@ __device__ __forceinline__ void tile_update_tri(double* DL, int off, int m, int 
 // INVERSE = false: DL holds L with its 8x8 diagonal tiles replaced by their inverses.
 // ------------------------------------------------------------------------------------------
 template <int NT, bool INVERSE = true>
-__device__ int potrf_trtri(double* DL, int* s_fail) {
+__device__ int potrf_trtri(double* DL, int* s_fail, unsigned long long* leaf_bars = nullptr) {
   using S = FactorShape<NT>;
   constexpr int LD = S::LD;
   constexpr int NWA = S::NWA;
@@ -307,13 +307,26 @@ __device__ int potrf_trtri(double* DL, int* s_fail) {
       if (lane == 0) *s_fail = f;
     } else if (p > 0) {
       // helpers: leaf of panel p-1, and panel p-1's update of the column blocks >= p+1
-      if (warp == 1 + (p - 1) % (NWA > 1 ? NWA - 1 : 1)) leaf_inverse<NT>(DL, p0 - 8, lane);
+      if (warp == 1 + (p - 1) % (NWA > 1 ? NWA - 1 : 1)) {
+        leaf_inverse<NT>(DL, p0 - 8, lane);
+        if (leaf_bars) {  // publish leaf p-1 (streaming consumers, btd_factor3.cuh)
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence_block();
+            mbar_arrive(&leaf_bars[p - 1]);
+          }
+        }
+      }
       tile_update_tri<NT, 4>(DL, p + 1, NP - p - 1, warp - 1, NWA - 1, p0 - 8, lane);
     }
     named_sync(kBarA, NWA * 32);
     BTD_PHASE(4);
     const int fail = *s_fail;
-    if (fail) return fail;
+    if (fail) {
+      if (leaf_bars && tid == 0)  // release the consumers of the leaves that will never come
+        for (int q = p; q < NP; ++q) mbar_arrive(&leaf_bars[q]);
+      return fail;
+    }
     // critical: panel p's update of column block p+1 (tiles (tr, p+1), tr >= p+1)
     for (int tr = p + 1 + warp; tr < NP; tr += NWA) tile_update<NT>(DL, tr, p + 1, p0, lane);
     if (NWA == 1 && p + 2 < NP)  // no helpers: the rest of panel p's update runs here
@@ -322,7 +335,17 @@ __device__ int potrf_trtri(double* DL, int* s_fail) {
     BTD_PHASE(5);
   }
   // remaining leaves: the last panel's (and all of them when group A is a single warp)
-  for (int lf = (NWA > 1 ? NP - 1 : 0) + warp; lf < NP; lf += NWA) leaf_inverse<NT>(DL, lf * 8, lane);
+  for (int lf = (NWA > 1 ? NP - 1 : 0) + warp; lf < NP; lf += NWA) {
+    leaf_inverse<NT>(DL, lf * 8, lane);
+    if (leaf_bars) {
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        mbar_arrive(&leaf_bars[lf]);
+      }
+    }
+  }
+  if (leaf_bars && !INVERSE) return 0;
   named_sync(kBarA, NWA * 32);
   BTD_PHASE(9);
   if (!INVERSE) return 0;

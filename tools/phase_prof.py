@@ -12,7 +12,7 @@ import paper_2509_03015_b200 as pkg
 L = _native.lib()
 L.btd_debug_phase_cycles.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
 names = {1: 'phase1', 2: 'pt_gemm', 3: 'D tiles', 4: 'panel chains', 5: 'crit tile upd',
-         9: 'leaves', 10: 'doubling', 11: 'pair potrf', 12: 'pair gemm', 13: 'pair phase', 14: 'p14', 15: 'p15'}
+         9: 'leaves', 10: 'doubling', 11: 'S potrf', 12: 'S B-pre (fill+SL)', 13: 'S B-trsm done', 14: 'S step', 15: 'p15'}
 for cfg in sys.argv[1:]:
     v = [int(x) for x in cfg.split(',')]
     N, n, d = v[:3]
