@@ -13,8 +13,10 @@ e2e        = same metric through the public API with pinned HOST buffers (H2D of
              D2H of X inside the timed region).
 roofline   = the dominant kernel (level-0 factor_level_kernel<64>), fp64 DMMA-bound, timed
              with CUDA events on the launching stream (C-ABI timing hook).
-Multi-GPU (torchrun): every rank runs its own instance (weak scaling, replicas) -- the sharded
-N = 2^20 path is reported separately by bench_sharded.
+Multi-GPU (torchrun, N > 1): the chain is sharded -- every rank owns a chunk of the
+configuration's size (weak scaling: N_global = N x chunk), eliminates its interiors locally and the
+reduced separator system is all-gathered over NCCL and solved redundantly; value = W_sub of the
+global chain / max-over-ranks time.
 """
 
 from __future__ import annotations
@@ -298,6 +300,127 @@ def run_ours(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------------------------------
+# N > 1: the sharded chain, weak scaling -- every rank owns a chunk of the
+# configuration's size, the reduced separator system is all-gathered over NCCL
+# ------------------------------------------------------------------------------------------
+def run_sharded(args, rank, world):
+    import torch
+    import torch.distributed as dist
+    from paper_2509_03015_b200 import sharded as sh
+    from paper_2509_03015_b200.synthgen import generate_spd_btd
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    cfg = args.config
+    N1, n, d = CONFIGS[cfg]
+    plan = sh.shard_plan(N1 * world, world)
+    a, b = plan.chunk(rank)
+    Nc = b - a + 1
+    # synthetic chunk: the reference generator's stream with seed = rank; the shared boundary
+    # block is owned by the left rank (diagonal shifted by n so it also dominates the right
+    # neighbour's coupling, |A_{b+1,b}| row sums <= n), the right rank passes zeros for it
+    hd = torch.empty((Nc, n, n), dtype=torch.float64).pin_memory()
+    hs = torch.empty((Nc - 1, n, n), dtype=torch.float64).pin_memory()
+    hb = torch.empty((Nc, n, d), dtype=torch.float64).pin_memory()
+    generate_spd_btd(Nc, n, d, seed=rank, out=(hd.numpy(), hs.numpy(), hb.numpy()))
+    if rank < world - 1:
+        hd[-1] += n * torch.eye(n, dtype=torch.float64)
+    if rank > 0:
+        hd[0] = 0.0
+        hb[0] = 0.0
+    dd, ds, db = hd.to(dev), hs.to(dev), hb.to(dev)
+    comm = sh.TorchComm()
+    solver = sh.ShardedSolver(plan, rank, comm, sh.CudaEngine(dev))
+
+    def step(d_, s_, b_):
+        solver.factorize(d_, s_)
+        x = solver.solve(b_)
+        solver.engine.release(solver.state)
+        return x
+
+    for _ in range(max(args.warmup, 3)):
+        x = step(dd, ds, db)
+    torch.cuda.synchronize()
+    # residual of this rank's interior rows (rows 1..Nc-2 only involve the chunk's own blocks)
+    from paper_2509_03015_b200 import report
+    y = report.btd_matmul(sh_matrix(dd, ds), sh_rhs(x)).blocks
+    r = (db[1:-1] - y[1:-1]).reshape(-1, d)
+    rres = float((torch.linalg.vector_norm(r, dim=0) / torch.linalg.vector_norm(db[1:-1].reshape(-1, d), dim=0)).max())
+    t = torch.tensor([rres], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    rres = float(t)
+
+    sampler = ClockSampler() if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    stream = torch.cuda.current_stream(dev)
+    from paper_2509_03015_b200 import _native
+    launches0 = _native.lib().btd_launch_count()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record(stream)
+    for _ in range(args.steps):
+        x = step(dd, ds, db)
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    launches = _native.lib().btd_launch_count() - launches0
+    ms = ev[0].elapsed_time(ev[1]) / args.steps
+    t = torch.tensor([ms], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t)
+    dist.barrier()
+    clocks = sampler.stop(dev.index) if sampler else None
+
+    # end to end: pinned host chunk -> device -> sharded factor + solve -> host solution chunk
+    hx = torch.empty_like(hb)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_steps = max(1, args.steps // 2)
+    for _ in range(e2e_steps):
+        xx = step(hd.to(dev, non_blocking=True), hs.to(dev, non_blocking=True), hb.to(dev, non_blocking=True))
+        hx.copy_(xx)
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    t = torch.tensor([e2e_ms], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t)
+    f, s_, _ = w_sub(plan.N, n, d)
+    if rank != 0:
+        return
+    line = {
+        "metric": "fp64 factor+solve GFLOP/s (W_sub), block-tridiagonal SPD N x n",
+        "value": round((f + s_) / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generate_spd_btd stream per chunk, seed=rank; inputs > L2, no flush)",
+        "config": {"workload": f"{cfg} chunk per GPU, sharded chain: N={plan.N} (={world} x ~{N1}) n={n} d={d}",
+                   "crossover": 64, "segment_length": 8, "parallelism": f"chain sharded x{world}",
+                   "local_levels": plan.L, "reduced_blocks": plan.reduced_N, "l2": "inputs larger than L2"},
+        "rel_residual_interior": rres, "w_sub_gflop": round((f + s_) / 1e9, 3),
+        "e2e": {"value": round((f + s_) / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s", "ms_per_step": round(e2e_ms, 3),
+                "h2d_bytes_per_step": int((hd.numel() + hs.numel() + hb.numel()) * 8) * world,
+                "d2h_bytes_per_step": int(hb.numel() * 8) * world},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "collective": "torch.distributed all_gather of the reduced separator system (factor) and rhs (solve)",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def sh_matrix(d, s):
+    from paper_2509_03015_b200.core import BlockTridiagonalMatrix
+    return BlockTridiagonalMatrix(d, s)
+
+
+def sh_rhs(x):
+    from paper_2509_03015_b200.core import BlockRhs
+    return BlockRhs(x)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -312,10 +435,13 @@ def main():
     if world > 1 and args.impl == "ours":
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
+        # BTD_BENCH_GLOO=1: host-staged gloo collectives (lets N ranks share one GPU for a dry run)
+        dist.init_process_group("gloo" if os.environ.get("BTD_BENCH_GLOO") == "1" else "nccl")
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif world > 1:
+        run_sharded(args, rank, world)
     else:
         run_ours(args, rank, world)
     if world > 1 and args.impl == "ours":

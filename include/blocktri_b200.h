@@ -137,6 +137,17 @@ int btd_solve_up(const btd_hierarchy* h, const double* rhs, const double* reduce
  * elapsed milliseconds of the last factorization's launches in that order. */
 int btd_profile_kernels(btd_hierarchy* h, int32_t enable);
 int btd_kernel_times(const btd_hierarchy* h, float* ms_out, int64_t cap, int64_t* count);
+/* Block SpMV y = A x (btd_matmul, core.py:280-288) and the fused residual of residual_report
+ * (report.py:20-38): norms2[c] = ||b_c - (A x)_c||_2^2, norms2[d + c] = ||b_c||_2^2, reduced in a
+ * fixed order (deterministic).  `workspace` holds btd_residual_workspace() bytes; norms2 is a
+ * device array of 2d doubles. */
+int btd_matmul(const double* diag, const double* sub, int64_t num_blocks, int64_t block_size, const double* x,
+               int64_t num_columns, double* y, void* stream, btd_status* st);
+int btd_residual_workspace(int64_t num_blocks, int64_t block_size, int64_t num_columns, size_t* bytes);
+int btd_residual_norms(const double* diag, const double* sub, int64_t num_blocks, int64_t block_size,
+                       const double* x, const double* b, int64_t num_columns, void* workspace, double* norms2,
+                       void* stream, btd_status* st);
+
 /* Process-wide count of kernels this library has launched (evidence for bench.py gpu_launches). */
 long long btd_launch_count(void);
 

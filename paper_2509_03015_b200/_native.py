@@ -35,6 +35,7 @@ EXPORTED_SYMBOLS = (
     "btd_num_levels", "btd_level_info", "btd_factor_workspace", "btd_factorize", "btd_check",
     "btd_solve_workspace", "btd_solve", "btd_level_factor", "btd_profile_kernels", "btd_kernel_times",
     "btd_create_partial", "btd_reduced_size", "btd_factorize_partial", "btd_solve_down", "btd_solve_up", "btd_launch_count",
+    "btd_matmul", "btd_residual_workspace", "btd_residual_norms",
 )
 
 
@@ -105,6 +106,9 @@ def lib() -> ctypes.CDLL:
         L.btd_solve_up.argtypes = [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, P(BtdStatus)]
         L.btd_kernel_times.argtypes = [c_vp, P(ctypes.c_float), c_i64, P(c_i64)]
         L.btd_launch_count.argtypes = []
+        L.btd_matmul.argtypes = [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, P(BtdStatus)]
+        L.btd_residual_workspace.argtypes = [c_i64, c_i64, c_i64, P(c_sz)]
+        L.btd_residual_norms.argtypes = [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, P(BtdStatus)]
         for name in EXPORTED_SYMBOLS:
             if name not in ("btd_version", "btd_default_config", "btd_destroy", "btd_launch_count"):
                 getattr(L, name).restype = ctypes.c_int

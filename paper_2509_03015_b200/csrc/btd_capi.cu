@@ -18,6 +18,7 @@
 #include "btd_solve.cuh"
 #include "btd_solve2.cuh"
 #include "btd_big.cuh"
+#include "btd_spmv.cuh"
 
 namespace {
 
@@ -1117,5 +1118,78 @@ int btd_kernel_times(const btd_hierarchy* h, float* ms_out, int64_t cap, int64_t
 }
 
 long long btd_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+// ---------------------------------------------------------------------------------------------
+// Block SpMV and fused residual norms (btd_spmv.cuh): btd_matmul bt/core.py:280-288,
+// residual_report bt/report.py:20-38.
+// ---------------------------------------------------------------------------------------------
+static void spmv_grid(int64_t N, int64_t d, long long* rows_per_cta, unsigned* ctas, unsigned* ycols) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long want = std::min<long long>(N, (long long)sms * 8);
+  *rows_per_cta = (N + want - 1) / want;
+  *ctas = (unsigned)((N + *rows_per_cta - 1) / *rows_per_cta);
+  *ycols = (unsigned)((d + btd::kSpmvMaxD - 1) / btd::kSpmvMaxD);
+}
+
+int btd_matmul(const double* diag, const double* sub, int64_t N, int64_t n, const double* x, int64_t d, double* y,
+               void* stream, btd_status* st) {
+  clear_status(st);
+  if (N < 1 || n < 1 || d < 1 || !diag || !x || !y || (N > 1 && !sub)) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_matmul: bad arguments");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  btd::SpmvArgs a{};
+  a.diag = diag;
+  a.sub = sub;
+  a.x = x;
+  a.y = y;
+  a.N = N;
+  a.n = (int)n;
+  a.d = (int)d;
+  unsigned ctas, ycols;
+  spmv_grid(N, d, &a.rows_per_cta, &ctas, &ycols);
+  btd::btd_spmv_kernel<<<dim3(ctas, ycols), btd::kSpmvThreads, 0, (cudaStream_t)stream>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(st, e, "btd_matmul");
+  return BTD_OK;
+}
+
+int btd_residual_workspace(int64_t N, int64_t n, int64_t d, size_t* bytes) {
+  (void)n;
+  if (N < 1 || d < 1 || !bytes) return BTD_ERR_INVALID_ARGUMENT;
+  long long rows;
+  unsigned ctas, ycols;
+  spmv_grid(N, d, &rows, &ctas, &ycols);
+  *bytes = (size_t)ctas * 2 * (size_t)d * sizeof(double);
+  return BTD_OK;
+}
+
+int btd_residual_norms(const double* diag, const double* sub, int64_t N, int64_t n, const double* x, const double* b,
+                       int64_t d, void* workspace, double* norms2, void* stream, btd_status* st) {
+  clear_status(st);
+  if (N < 1 || n < 1 || d < 1 || !diag || !x || !b || !workspace || !norms2 || (N > 1 && !sub)) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_residual_norms: bad arguments");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  btd::SpmvArgs a{};
+  a.diag = diag;
+  a.sub = sub;
+  a.x = x;
+  a.b = b;
+  a.partial = (double*)workspace;
+  a.N = N;
+  a.n = (int)n;
+  a.d = (int)d;
+  unsigned ctas, ycols;
+  spmv_grid(N, d, &a.rows_per_cta, &ctas, &ycols);
+  cudaStream_t s = (cudaStream_t)stream;
+  btd::btd_spmv_kernel<<<dim3(ctas, ycols), btd::kSpmvThreads, 0, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
+  btd::btd_norm_finish_kernel<<<(unsigned)((2 * d + 127) / 128), 128, 0, s>>>(a.partial, (int)ctas, (int)d, norms2); g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(st, e, "btd_residual_norms");
+  return BTD_OK;
+}
 
 }  // extern "C"

@@ -277,6 +277,8 @@ class TorchComm:
         import torch
         if isinstance(x, np.ndarray):  # CPU engines (gloo tests)
             return [o.numpy() for o in self.all_gather_blocks(torch.from_numpy(np.ascontiguousarray(x)), counts)]
+        if x.is_cuda and self.dist.get_backend(self.group) == "gloo":  # gloo: stage through the host
+            return [o.to(x.device) for o in self.all_gather_blocks(x.cpu(), counts)]
         m = max(counts)
         pad = torch.zeros((m,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
         pad[:x.shape[0]] = x
