@@ -132,6 +132,15 @@ int btd_solve_down(const btd_hierarchy* h, const double* rhs, double* x, int64_t
 int btd_solve_up(const btd_hierarchy* h, const double* rhs, const double* reduced_x, double* x, int64_t num_columns,
                  void* scratch, void* stream, btd_status* st);
 
+/* btd_factorize with HOST-resident inputs (pinned for full overlap): the blocks are copied into the
+ * caller's device arrays dev_diag / dev_sub in chunks of whole level-0 segments on a private copy
+ * stream, and every chunk is eliminated as soon as it has landed (H2D overlaps the level-0 factor).
+ * Same result and errors as btd_factorize(h, dev_diag, dev_sub, ...); the host arrays are read
+ * asynchronously until the work on `stream` completes. */
+int btd_factorize_from_host(btd_hierarchy* h, const double* host_diag, const double* host_sub, double* dev_diag,
+                            double* dev_sub, void* persistent, void* scratch, void* stream, int32_t check,
+                            btd_status* st);
+
 /* Optional per-launch timing: when enabled, btd_factorize records CUDA events on the caller's
  * stream around every factor kernel (one per level, then the base).  btd_kernel_times returns the
  * elapsed milliseconds of the last factorization's launches in that order. */

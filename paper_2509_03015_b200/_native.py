@@ -13,6 +13,8 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libblocktri_b200.so")
+if os.environ.get("BTD_LIB"):  # developer A/B builds (tools/); the shipped library is LIB_PATH
+    LIB_PATH = os.path.abspath(os.environ["BTD_LIB"])
 _SOURCES = sorted(os.path.join(_HERE, "csrc", f) for f in os.listdir(os.path.join(_HERE, "csrc"))
                   if f.endswith((".cu", ".cuh"))) + \
            [os.path.join(os.path.dirname(_HERE), "include", "blocktri_b200.h")]
@@ -35,7 +37,7 @@ EXPORTED_SYMBOLS = (
     "btd_num_levels", "btd_level_info", "btd_factor_workspace", "btd_factorize", "btd_check",
     "btd_solve_workspace", "btd_solve", "btd_level_factor", "btd_profile_kernels", "btd_kernel_times",
     "btd_create_partial", "btd_reduced_size", "btd_factorize_partial", "btd_solve_down", "btd_solve_up", "btd_launch_count",
-    "btd_matmul", "btd_residual_workspace", "btd_residual_norms",
+    "btd_matmul", "btd_residual_workspace", "btd_residual_norms", "btd_factorize_from_host",
 )
 
 
@@ -106,6 +108,7 @@ def lib() -> ctypes.CDLL:
         L.btd_solve_up.argtypes = [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, P(BtdStatus)]
         L.btd_kernel_times.argtypes = [c_vp, P(ctypes.c_float), c_i64, P(c_i64)]
         L.btd_launch_count.argtypes = []
+        L.btd_factorize_from_host.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, P(BtdStatus)]
         L.btd_matmul.argtypes = [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, P(BtdStatus)]
         L.btd_residual_workspace.argtypes = [c_i64, c_i64, c_i64, P(c_sz)]
         L.btd_residual_norms.argtypes = [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, P(BtdStatus)]

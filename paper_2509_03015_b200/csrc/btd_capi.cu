@@ -61,8 +61,10 @@ struct btd_hierarchy {
   bool profile = false;
   std::vector<cudaEvent_t> ev;
   int nev = 0;
+  cudaStream_t copy_stream = nullptr;  // btd_factorize_from_host
   ~btd_hierarchy() {
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
   }
 };
 
@@ -694,8 +696,66 @@ int btd_factor_workspace(const btd_hierarchy* h, size_t* persistent_bytes, size_
   return BTD_OK;
 }
 
+struct HostSrc {
+  const double* diag;
+  const double* sub;
+  double* dev_diag;
+  double* dev_sub;
+};
+
+cudaError_t chunked_level0(btd_hierarchy* h, btd::FactorArgs a, const LevelPlan& lp, const HostSrc& src,
+                           cudaStream_t stream) {
+  if (!h->copy_stream) {
+    cudaError_t e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return e;
+  }
+  const size_t nn = (size_t)h->n * h->n;
+  const int64_t K = lp.K;
+  const int64_t chunks = std::min<int64_t>(K, 16);
+  // the copy stream must not overwrite buffers a previous factorization on `stream` still reads
+  cudaEvent_t ready;
+  cudaError_t e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+  if (e != cudaSuccess) return e;
+  cudaEventRecord(ready, stream);
+  cudaStreamWaitEvent(h->copy_stream, ready, 0);
+  cudaEventDestroy(ready);
+  int64_t row0 = 0;
+  for (int64_t c = 0; c < chunks; ++c) {
+    const int64_t ka = K * c / chunks, kb = K * (c + 1) / chunks;
+    // segments [ka, kb) read diag/sub rows up to seps[kb] (exclusive for sub, inclusive for the
+    // separator diag read by the assembly); the last chunk takes everything that is left
+    const int64_t row1 = (c + 1 == chunks) ? lp.N : lp.seps[kb] + 1;
+    e = cudaMemcpyAsync(src.dev_diag + row0 * nn, src.diag + row0 * nn, (size_t)(row1 - row0) * nn * sizeof(double),
+                        cudaMemcpyHostToDevice, h->copy_stream);
+    const int64_t srow1 = std::min<int64_t>(row1, lp.N - 1);
+    if (e == cudaSuccess && srow1 > row0)
+      e = cudaMemcpyAsync(src.dev_sub + row0 * nn, src.sub + row0 * nn, (size_t)(srow1 - row0) * nn * sizeof(double),
+                          cudaMemcpyHostToDevice, h->copy_stream);
+    if (e != cudaSuccess) return e;
+    cudaEvent_t ev;
+    e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    cudaEventRecord(ev, h->copy_stream);
+    cudaStreamWaitEvent(stream, ev, 0);
+    cudaEventDestroy(ev);
+    btd::FactorArgs ac = a;
+    ac.k0 = (int)ka;
+    if (kb > ka) {
+      e = dispatch_factor(h->nt, ac, (unsigned)(kb - ka), stream);
+      if (e != cudaSuccess) return e;
+    }
+    row0 = row1;
+  }
+  return cudaSuccess;
+}
+
+// Host-resident input (btd_factorize_from_host): the level-0 blocks are copied in chunks of whole
+// segments on a private copy stream, and each chunk's segments are factored as soon as their
+// blocks have landed, so the H2D transfer overlaps the level-0 elimination.
+
 static int factorize_impl(btd_hierarchy* h, const double* diag, const double* sub, void* persistent, void* scratch,
-                          void* stream_, int32_t check, btd_status* st, double* red_diag, double* red_sub) {
+                          void* stream_, int32_t check, btd_status* st, double* red_diag, double* red_sub,
+                          const HostSrc* host = nullptr) {
   clear_status(st);
   if (!h || !diag || !persistent || !scratch || (h->N > 1 && !sub)) {
     set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_factorize: NULL argument");
@@ -723,6 +783,14 @@ static int factorize_impl(btd_hierarchy* h, const double* diag, const double* su
   if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(seps)");
   h->nev = 0;
 
+  if (host && (h->big || h->levels.empty())) {  // no chunking: one bulk copy, then the usual path
+    const size_t nn = (size_t)h->n * h->n * sizeof(double);
+    e = cudaMemcpyAsync(host->dev_diag, host->diag, (size_t)h->N * nn, cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess && h->N > 1)
+      e = cudaMemcpyAsync(host->dev_sub, host->sub, (size_t)(h->N - 1) * nn, cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize_from_host(copy)");
+    host = nullptr;
+  }
   const double* cd = diag;
   const double* cs = sub;
   if (h->big) {
@@ -777,10 +845,17 @@ static int factorize_impl(btd_hierarchy* h, const double* diag, const double* su
     a.Sr = (double*)(scr + lp.off_sr);
     a.Ssub = (double*)(scr + lp.off_next_sub);
     a.err = err;
-    prof_mark(h, stream);
-    e = dispatch_factor(h->nt, a, (unsigned)lp.K, stream);
-    prof_mark(h, stream);
-    if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(level kernel)");
+    if (l == 0 && host) {
+      prof_mark(h, stream);
+      e = chunked_level0(h, a, lp, *host, stream);
+      prof_mark(h, stream);
+      if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize_from_host(level 0)");
+    } else {
+      prof_mark(h, stream);
+      e = dispatch_factor(h->nt, a, (unsigned)lp.K, stream);
+      prof_mark(h, stream);
+      if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(level kernel)");
+    }
     btd::assemble_schur_diag_kernel<<<(unsigned)lp.P, 256, 0, stream>>>(cd, a.seps, a.Sl, a.Sr, (int)lp.K, n, err); g_launches.fetch_add(1, std::memory_order_relaxed);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(assemble)");
@@ -820,6 +895,17 @@ int btd_factorize(btd_hierarchy* h, const double* diag, const double* sub, void*
     return BTD_ERR_INVALID_ARGUMENT;
   }
   return factorize_impl(h, diag, sub, persistent, scratch, stream, check, st, nullptr, nullptr);
+}
+
+int btd_factorize_from_host(btd_hierarchy* h, const double* host_diag, const double* host_sub, double* dev_diag,
+                            double* dev_sub, void* persistent, void* scratch, void* stream, int32_t check,
+                            btd_status* st) {
+  if (!h || h->partial || !host_diag || !dev_diag || (h->N > 1 && (!host_sub || !dev_sub))) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_factorize_from_host: bad arguments");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  HostSrc src{host_diag, host_sub, dev_diag, dev_sub};
+  return factorize_impl(h, dev_diag, dev_sub, persistent, scratch, stream, check, st, nullptr, nullptr, &src);
 }
 
 int btd_factorize_partial(btd_hierarchy* h, const double* diag, const double* sub, void* persistent, void* scratch,

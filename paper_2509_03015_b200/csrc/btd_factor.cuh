@@ -48,6 +48,7 @@ struct FactorArgs {
   long long N;
   int n;
   int K;        // segments (base: 1)
+  int k0;       // first segment of this launch (blockIdx.x = k - k0): chunked level-0 launches
   int base;     // 1: serial base case, the whole chain is one uncoupled segment
   int level;
   double* Linv;  // (N, packed) out: inverse Cholesky factor of every interior row, packed lower
@@ -345,10 +346,12 @@ __device__ int potrf_trtri(double* DL, int* s_fail, unsigned long long* leaf_bar
       }
     }
   }
-  if (leaf_bars && !INVERSE) return 0;
+  if constexpr (!INVERSE) {
+    if (!leaf_bars) named_sync(kBarA, NWA * 32);
+    return 0;
+  } else {
   named_sync(kBarA, NWA * 32);
   BTD_PHASE(9);
-  if (!INVERSE) return 0;
 
   // ---- recursive doubling: [[A,0],[B,C]]^{-1} = [[Ai,0],[-Ci B Ai, Ci]] on DMMA ----
 #pragma unroll
@@ -407,6 +410,7 @@ __device__ int potrf_trtri(double* DL, int* s_fail, unsigned long long* leaf_bar
   }
   BTD_PHASE(10);
   return 0;
+  }
 }
 
 // Pt = Xt * Linv^T, in place on the XP rows owned by this warp (16 rows per warp, two 8-row passes:
@@ -554,8 +558,8 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
   double* DL = smem + 2 * NT * LD;  // NT x LD  : D -> L -> Linv
   __shared__ int s_fail;
 
-  if (npd_superseded(args.err, args.level, 0, blockIdx.x)) return;
-  const int k = blockIdx.x;
+  const int k = args.k0 + blockIdx.x;
+  if (npd_superseded(args.err, args.level, 0, k)) return;
   const bool coupled = !args.base;
   const long long start = coupled ? (long long)args.seps[k] + 1 : 0;
   const long long stop = coupled ? (long long)args.seps[k + 1] : args.N;

@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(StreamShape::NTHREADS, 1) factor_stream_kernel
   __shared__ __align__(8) unsigned long long leaf_bar[8];
   __shared__ int s_fail_a, s_fail;
 
-  const int k = blockIdx.x;
+  const int k = args.k0 + blockIdx.x;
   if (npd_superseded(args.err, args.level, 0, k)) return;
   const bool coupled = !args.base;
   const long long start = coupled ? (long long)args.seps[k] + 1 : 0;

@@ -439,7 +439,10 @@ struct TmaShape {
   using S = Solve2Shape<NT>;
   static constexpr int NCW = S::NTHREADS / 32;  // consumer warps
   static constexpr int NTHREADS = S::NTHREADS + 32;
-  static constexpr int STAGES = NT == 64 ? (DC > 1 ? 3 : 4) : 8;
+#ifndef BTD_TMA_STAGES64
+#define BTD_TMA_STAGES64 4
+#endif
+  static constexpr int STAGES = NT == 64 ? (DC > 1 ? 3 : BTD_TMA_STAGES64) : 8;
   static constexpr int STAGE = S::FULL + S::PACK + NT * DC;  // doubles per slot
   static constexpr size_t SMEM = sizeof(double) * ((size_t)STAGES * STAGE + (size_t)(4 + S::ZMAX + S::PARTS) * NT * DC) +
                                  2 * STAGES * sizeof(unsigned long long);

@@ -144,6 +144,25 @@ def _device_matrix(matrix: BlockTridiagonalMatrix):
     return diag, sub
 
 
+def _host_matrix(matrix: BlockTridiagonalMatrix):
+    """(diag ptr, sub ptr, keep-alive) for host-resident float64 contiguous arenas, else None."""
+    N, n = matrix.num_blocks, matrix.block_size
+    if _is_torch(matrix.diag):
+        if matrix.diag.device.type != "cpu":
+            return None
+        import torch
+        d = matrix.diag.to(torch.float64).contiguous()
+        s = matrix.sub.to(torch.float64).contiguous()
+        if tuple(d.shape) != (N, n, n) or tuple(s.shape) != (max(N - 1, 0), n, n):
+            raise DimensionMismatch(f"matrix arenas {tuple(d.shape)}, {tuple(s.shape)} do not match (N={N}, n={n})")
+        return d.data_ptr(), s.data_ptr(), (d, s)
+    d = np.ascontiguousarray(matrix.diag, dtype=np.float64)
+    s = np.ascontiguousarray(matrix.sub, dtype=np.float64)
+    if d.shape != (N, n, n) or s.shape != (max(N - 1, 0), n, n):
+        raise DimensionMismatch(f"matrix arenas {d.shape}, {s.shape} do not match (N={N}, n={n})")
+    return d.ctypes.data, s.ctypes.data, (d, s)
+
+
 def recursive_factorize(matrix: BlockTridiagonalMatrix, config: RecursionConfig | None = None,
                         *, stream=None, profile: bool = False) -> FactorHierarchy:
     """Factor an SPD block-tridiagonal system for repeated solves (schur.py:289-318).
@@ -161,7 +180,12 @@ def recursive_factorize(matrix: BlockTridiagonalMatrix, config: RecursionConfig 
     rc = L.btd_create(N, n, ctypes.byref(c), ctypes.byref(handle), ctypes.byref(st))
     if rc != _native.BTD_OK:
         _raise_status(st, rc)
-    diag, sub = _device_matrix(matrix)
+    host = _host_matrix(matrix)
+    if host is None:
+        diag, sub = _device_matrix(matrix)
+    else:  # host-resident input: the C ABI overlaps the H2D copy with the level-0 elimination
+        diag = torch.empty((N, n, n), dtype=torch.float64, device="cuda")
+        sub = torch.empty((max(N - 1, 0), n, n), dtype=torch.float64, device="cuda")
     pers_b, scr_b = ctypes.c_size_t(), ctypes.c_size_t()
     L.btd_factor_workspace(handle, ctypes.byref(pers_b), ctypes.byref(scr_b))
     dev = diag.device
@@ -171,8 +195,14 @@ def recursive_factorize(matrix: BlockTridiagonalMatrix, config: RecursionConfig 
     if profile:
         L.btd_profile_kernels(handle, 1)
     s = stream if stream is not None else torch.cuda.current_stream(dev)
-    rc = L.btd_factorize(handle, diag.data_ptr(), sub.data_ptr() if N > 1 else None, persistent.data_ptr(),
-                         scratch.data_ptr(), ctypes.c_void_p(s.cuda_stream), 1, ctypes.byref(st))
+    if host is None:
+        rc = L.btd_factorize(handle, diag.data_ptr(), sub.data_ptr() if N > 1 else None, persistent.data_ptr(),
+                             scratch.data_ptr(), ctypes.c_void_p(s.cuda_stream), 1, ctypes.byref(st))
+    else:
+        hd, hs, _keep = host
+        rc = L.btd_factorize_from_host(handle, hd, hs if N > 1 else None, diag.data_ptr(),
+                                       sub.data_ptr() if N > 1 else None, persistent.data_ptr(),
+                                       scratch.data_ptr(), ctypes.c_void_p(s.cuda_stream), 1, ctypes.byref(st))
     del scratch
     if rc != _native.BTD_OK:
         _raise_status(st, rc)
@@ -206,7 +236,7 @@ def recursive_solve(hierarchy: FactorHierarchy, rhs: BlockRhs, *, stream=None) -
     host = not _is_torch(rhs.blocks)
     host_tensor = (not host) and rhs.blocks.device.type == "cpu"
     if host:
-        b = torch.from_numpy(np.ascontiguousarray(rhs.blocks, dtype=np.float64)).to(native.device)
+        b = torch.from_numpy(np.ascontiguousarray(rhs.blocks, dtype=np.float64)).to(native.device, non_blocking=True)
     else:
         b = rhs.blocks
         if b.device != native.device:
@@ -223,10 +253,13 @@ def recursive_solve(hierarchy: FactorHierarchy, rhs: BlockRhs, *, stream=None) -
                      ctypes.c_void_p(s.cuda_stream), ctypes.byref(st))
     if rc != _native.BTD_OK:
         _raise_status(st, rc)
-    if host:
-        return BlockRhs(x.cpu().numpy())
-    if host_tensor:
-        return BlockRhs(x.cpu())
+    if host or host_tensor:
+        # D2H into pinned memory (torch's caching host allocator): a pageable destination runs at a
+        # fraction of the link bandwidth
+        out = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        out.copy_(x, non_blocking=True)
+        s.synchronize()
+        return BlockRhs(out.numpy() if host else out)
     return BlockRhs(x)
 
 

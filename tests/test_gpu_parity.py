@@ -158,3 +158,29 @@ def test_sharded_gpu_matches_unsharded(case):
     assert rel <= 1e-12, rel
     _, rres = pkg.residual_report(dA, pkg.BlockRhs(X), dB)
     assert rres <= REL_RES
+
+
+@pytest.mark.parametrize("N,n,d", [(4096, 64, 1), (20000, 8, 2), (3000, 33, 1), (600, 128, 2)])
+def test_host_input_overlapped_copy_is_bitwise_device_path(N, n, d):
+    """btd_factorize_from_host (chunked H2D overlapping the level-0 kernels) == device-input path."""
+    A, B = pkg.generate_spd_btd(N, n, d, seed=11)
+    dA = pkg.BlockTridiagonalMatrix(torch.from_numpy(A.diag).cuda(), torch.from_numpy(A.sub).cuda())
+    dB = pkg.BlockRhs(torch.from_numpy(B.blocks).cuda())
+    x_dev = pkg.recursive_solve(pkg.recursive_factorize(dA), dB).blocks.cpu().numpy()
+    x_np = pkg.recursive_solve(pkg.recursive_factorize(A), B).blocks
+    pA = pkg.BlockTridiagonalMatrix(torch.from_numpy(A.diag).pin_memory(), torch.from_numpy(A.sub).pin_memory())
+    x_pin = pkg.recursive_solve(pkg.recursive_factorize(pA), dB).blocks.cpu().numpy()
+    assert np.array_equal(x_dev, x_np) and np.array_equal(x_dev, x_pin)
+
+
+def test_host_input_npd_coordinates_match_device_path():
+    A, _ = pkg.generate_spd_btd(5000, 16, 1, seed=2)
+    diag = A.diag.copy()
+    diag[2345, 3, 3] = -50.0
+    bad = pkg.BlockTridiagonalMatrix(diag, A.sub)
+    with pytest.raises(pkg.NotPositiveDefinite) as e_host:
+        pkg.recursive_factorize(bad)
+    with pytest.raises(pkg.NotPositiveDefinite) as e_dev:
+        pkg.recursive_factorize(pkg.BlockTridiagonalMatrix(torch.from_numpy(diag).cuda(), torch.from_numpy(A.sub).cuda()))
+    a, b = e_host.value, e_dev.value
+    assert (a.pivot, a.level, a.member, a.block) == (b.pivot, b.level, b.member, b.block)
