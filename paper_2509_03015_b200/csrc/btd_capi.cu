@@ -131,6 +131,18 @@ bool should_recurse(int64_t N, const btd_config& cfg) {
   return N > cfg.crossover;
 }
 
+// grid of a flattened grid-stride elementwise kernel (256 threads per CTA)
+unsigned flat_grid(int64_t elements) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t want = (elements + 255) / 256;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 16));
+}
+
 int pick_nt(int64_t n) {
   if (n <= 8) return 8;
   if (n <= 16) return 16;
@@ -806,7 +818,7 @@ static int factorize_impl(btd_hierarchy* h, const double* diag, const double* su
                            scr + h->off_big_ws, err);
       prof_mark(h, stream);
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(big level)");
-      btd::assemble_schur_diag_kernel<<<(unsigned)lp.P, 256, 0, stream>>>(
+      btd::assemble_schur_diag_kernel<<<flat_grid(lp.P * h->n * h->n), 256, 0, stream>>>(
           cd, (const int*)(pers + lp.off_seps), next_diag, (const double*)(scr + lp.off_sr), (int)lp.K, n, err); g_launches.fetch_add(1, std::memory_order_relaxed);
       e = cudaGetLastError();
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(assemble)");
@@ -856,7 +868,7 @@ static int factorize_impl(btd_hierarchy* h, const double* diag, const double* su
       prof_mark(h, stream);
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(level kernel)");
     }
-    btd::assemble_schur_diag_kernel<<<(unsigned)lp.P, 256, 0, stream>>>(cd, a.seps, a.Sl, a.Sr, (int)lp.K, n, err); g_launches.fetch_add(1, std::memory_order_relaxed);
+    btd::assemble_schur_diag_kernel<<<flat_grid(lp.P * h->n * h->n), 256, 0, stream>>>(cd, a.seps, a.Sl, a.Sr, (int)lp.K, n, err); g_launches.fetch_add(1, std::memory_order_relaxed);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(assemble)");
     cd = a.Sl;
@@ -1002,7 +1014,7 @@ static int solve_impl(const btd_hierarchy* h, const double* rhs, double* x, int6
       e = big_solve_level(c, btd::kSolveDown, jmax, n, dd, rhs_l[l], (const double*)(pers + lp.off_linv),
                           (const double*)(pers + lp.off_lsub), x_l[l], nullptr, rhs_l[l + 1], fr_l[l], Tws, Uws);
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(big down)");
-      btd::assemble_separator_rhs_kernel<<<(unsigned)lp.P, 128, 0, stream>>>(rhs_l[l], sp, rhs_l[l + 1], fr_l[l],
+      btd::assemble_separator_rhs_kernel<<<flat_grid(lp.P * h->n * d), 256, 0, stream>>>(rhs_l[l], sp, rhs_l[l + 1], fr_l[l],
                                                                               (int)lp.K, n, dd, err); g_launches.fetch_add(1, std::memory_order_relaxed);
       e = cudaGetLastError();
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(assemble)");
@@ -1069,7 +1081,7 @@ static int solve_impl(const btd_hierarchy* h, const double* rhs, double* x, int6
     a.err = err;
     e = (n == h->nt) ? dispatch_stream(h->nt, a, stream) : dispatch_solve(h->nt, a, (unsigned)lp.K, stream);
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(down)");
-    btd::assemble_separator_rhs_kernel<<<(unsigned)lp.P, 128, 0, stream>>>(rhs_l[l], a.seps, rhs_l[l + 1], fr_l[l],
+    btd::assemble_separator_rhs_kernel<<<flat_grid(lp.P * h->n * d), 256, 0, stream>>>(rhs_l[l], a.seps, rhs_l[l + 1], fr_l[l],
                                                                             (int)lp.K, n, (int)d, err); g_launches.fetch_add(1, std::memory_order_relaxed);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(assemble)");

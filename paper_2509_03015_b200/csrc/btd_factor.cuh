@@ -78,7 +78,7 @@ struct FactorShape {
   static constexpr int MAXD = (ND + NW - 1) / NW;
   static constexpr int MAXV = (NT * NT / 256 + NWA - 1) / NWA > 0 ? (NT * NT / 256 + NWA - 1) / NWA : 1;
   static constexpr size_t SMEM = (size_t)3 * NT * LD * sizeof(double);
-  static constexpr int MINB = NT == 64 ? 2 : NT == 32 ? 4 : 8;  // CTAs per SM to overlap pivot latency
+  static constexpr int MINB = NT == 64 ? 2 : NT == 32 ? 4 : NT == 16 ? 8 : 16;  // CTAs per SM (NT = 8: 124 regs, no spills)
   static_assert(NT / 8 == NW, "one trtri leaf per warp");
   static_assert(NWB == 0 || 16 * NWB == NT, "group B owns 16 rows of the fill block per warp");
 };
@@ -701,18 +701,19 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
 __global__ void assemble_schur_diag_kernel(const double* diag, const int* seps, double* next_diag,
                                            const double* Sr, int K, int n, const DevErr* err) {
   if (error_raised(err)) return;
-  const int p = blockIdx.x;
+  // flattened grid-stride over P blocks x n^2 elements (a CTA per separator wastes most threads
+  // at small n: 116510 separators x 64 elements at n = 8)
   const size_t bs = (size_t)n * n;
-  const double* a = diag + (size_t)seps[p] * bs;
-  double* out = next_diag + (size_t)p * bs;
-  const double* sr = p > 0 ? Sr + (size_t)(p - 1) * bs : nullptr;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int r = e / n, c = e % n;
+  const size_t total = (size_t)(K + 1) * bs;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int p = (int)(e / bs);
+    const int i = (int)(e % bs);
+    const int r = i / n, c = i % n;
     if (c > r) continue;
-    double v = a[e];
-    if (p < K) v -= out[e];
-    if (sr) v -= sr[e];
-    out[e] = v;
+    double v = diag[(size_t)seps[p] * bs + i];
+    if (p < K) v -= next_diag[e];
+    if (p > 0) v -= Sr[e - bs];
+    next_diag[e] = v;
   }
 }
 

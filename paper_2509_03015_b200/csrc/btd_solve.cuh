@@ -204,15 +204,14 @@ __global__ void __launch_bounds__(SolveShape<NT>::NTHREADS) solve_level_kernel(S
 __global__ void assemble_separator_rhs_kernel(const double* rhs, const int* seps, double* next_rhs,
                                               const double* fr, int K, int n, int d, const DevErr* err) {
   if (error_raised(err)) return;
-  const int p = blockIdx.x;
   const size_t ps = (size_t)n * d;
-  const double* b = rhs + (size_t)seps[p] * ps;
-  double* out = next_rhs + (size_t)p * ps;
-  for (int e = threadIdx.x; e < (int)ps; e += blockDim.x) {
-    double v = b[e];
-    if (p < K) v -= out[e];
-    if (p > 0) v -= fr[(size_t)(p - 1) * ps + e];
-    out[e] = v;
+  const size_t total = (size_t)(K + 1) * ps;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int p = (int)(e / ps);
+    double v = rhs[(size_t)seps[p] * ps + e % ps];
+    if (p < K) v -= next_rhs[e];
+    if (p > 0) v -= fr[e - ps];
+    next_rhs[e] = v;
   }
 }
 
