@@ -19,6 +19,7 @@
 #include "btd_solve2.cuh"
 #include "btd_big.cuh"
 #include "btd_spmv.cuh"
+#include "btd_small.cuh"
 
 namespace {
 
@@ -200,7 +201,23 @@ cudaError_t launch_stream64(const btd::FactorArgs& a, unsigned grid, cudaStream_
   return cudaGetLastError();
 }
 
+// Register-resident small-block kernel (btd_small.cuh) at NT = 8; BTD_SMALL=0 falls back to
+// factor_level_kernel<8> (A/B timing).
+bool use_small(int nt) {
+  static int env = -1;
+  if (env < 0) {
+    const char* v = getenv("BTD_SMALL");
+    env = (v && v[0] == '0') ? 0 : 1;
+  }
+  return env && nt == 8;
+}
+
 cudaError_t dispatch_factor(int nt, const btd::FactorArgs& a, unsigned grid, cudaStream_t s) {
+  if (use_small(nt)) {
+    const unsigned g = a.base ? 1u : (grid + 15) / 16;
+    btd::factor_small_kernel<<<g, btd::kSmallThreads, 0, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+  }
   if (use_stream(nt, a)) return launch_stream64(a, grid, s);
   switch (nt) {
     case 8: return launch_factor<8>(a, grid, s);
@@ -263,6 +280,17 @@ cudaError_t dispatch_stream(int nt, const btd::SolveArgs& a, cudaStream_t s) {
     case 64: return dispatch_stream_dc<64>(a, s);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_solve_small(const btd::SolveArgs& a, cudaStream_t s) {
+  const unsigned gx = a.mode == btd::kSolveBase ? 1u : (unsigned)((a.K + 15) / 16);
+  const int dc = a.d == 1 ? 1 : a.d == 2 ? 2 : 4;
+  dim3 grid(gx, (unsigned)((a.d + dc - 1) / dc));
+  if (dc == 1) btd::solve_small_kernel<1><<<grid, btd::kSmallThreads, 0, s>>>(a);
+  else if (dc == 2) btd::solve_small_kernel<2><<<grid, btd::kSmallThreads, 0, s>>>(a);
+  else btd::solve_small_kernel<4><<<grid, btd::kSmallThreads, 0, s>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
 }
 
 cudaError_t dispatch_solve(int nt, const btd::SolveArgs& a, unsigned grid_x, cudaStream_t s) {
@@ -752,6 +780,7 @@ cudaError_t chunked_level0(btd_hierarchy* h, btd::FactorArgs a, const LevelPlan&
     cudaEventDestroy(ev);
     btd::FactorArgs ac = a;
     ac.k0 = (int)ka;
+    ac.kend = (int)kb;
     if (kb > ka) {
       e = dispatch_factor(h->nt, ac, (unsigned)(kb - ka), stream);
       if (e != cudaSuccess) return e;
@@ -1079,7 +1108,7 @@ static int solve_impl(const btd_hierarchy* h, const double* rhs, double* x, int6
     a.K = (int)lp.K;
     a.mode = btd::kSolveDown;
     a.err = err;
-    e = (n == h->nt) ? dispatch_stream(h->nt, a, stream) : dispatch_solve(h->nt, a, (unsigned)lp.K, stream);
+    e = use_small(h->nt) ? launch_solve_small(a, stream) : (n == h->nt) ? dispatch_stream(h->nt, a, stream) : dispatch_solve(h->nt, a, (unsigned)lp.K, stream);
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(down)");
     btd::assemble_separator_rhs_kernel<<<flat_grid(lp.P * h->n * d), 256, 0, stream>>>(rhs_l[l], a.seps, rhs_l[l + 1], fr_l[l],
                                                                             (int)lp.K, n, (int)d, err); g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -1105,7 +1134,7 @@ static int solve_impl(const btd_hierarchy* h, const double* rhs, double* x, int6
     a.K = 1;
     a.mode = btd::kSolveBase;
     a.err = err;
-    e = (n == h->nt) ? dispatch_stream(h->nt, a, stream) : dispatch_solve(h->nt, a, 1u, stream);
+    e = use_small(h->nt) ? launch_solve_small(a, stream) : (n == h->nt) ? dispatch_stream(h->nt, a, stream) : dispatch_solve(h->nt, a, 1u, stream);
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(base)");
   }
   for (size_t l = L; l-- > 0;) {
@@ -1123,7 +1152,7 @@ static int solve_impl(const btd_hierarchy* h, const double* rhs, double* x, int6
     a.K = (int)lp.K;
     a.mode = btd::kSolveUp;
     a.err = err;
-    e = (n == h->nt) ? dispatch_stream(h->nt, a, stream) : dispatch_solve(h->nt, a, (unsigned)lp.K, stream);
+    e = use_small(h->nt) ? launch_solve_small(a, stream) : (n == h->nt) ? dispatch_stream(h->nt, a, stream) : dispatch_solve(h->nt, a, (unsigned)lp.K, stream);
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(up)");
   }
   return BTD_OK;

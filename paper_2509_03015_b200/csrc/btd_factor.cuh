@@ -49,6 +49,7 @@ struct FactorArgs {
   int n;
   int K;        // segments (base: 1)
   int k0;       // first segment of this launch (blockIdx.x = k - k0): chunked level-0 launches
+  int kend;     // one past the last segment of this launch (0: K)
   int base;     // 1: serial base case, the whole chain is one uncoupled segment
   int level;
   double* Linv;  // (N, packed) out: inverse Cholesky factor of every interior row, packed lower
