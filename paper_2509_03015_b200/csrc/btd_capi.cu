@@ -33,7 +33,13 @@ struct LevelPlan {
   int64_t N = 0;  // blocks of this level's matrix
   int64_t P = 0;  // separators (= blocks of the next level)
   int64_t K = 0;  // segments
-  std::vector<int64_t> seps;
+  int64_t step = 0;  // rho + 1: separators are k * step (k < P-1) and N-1 (plan_partition, closed form)
+  int64_t sep(int64_t k) const { return k == P - 1 ? N - 1 : k * step; }
+  int64_t max_segment() const {  // longest segment (the tail absorbs the gap)
+    if (K < 1) return 0;
+    const int64_t regular = K > 1 ? step - 1 : 0;
+    return std::max(regular, sep(K) - sep(K - 1) - 1);
+  }
   // persistent offsets
   size_t off_seps = 0, off_linv = 0, off_lsub = 0;
   // factor-scratch offsets: next level matrix + S_R scratch
@@ -115,9 +121,10 @@ bool config_ok(const btd_config* c) {
 // plan_partition (bt/schur.py:75-95): separators at 0, rho+1, 2(rho+1), ...; the last block is always
 // a separator; a regular separator adjacent to it is dropped so the tail segment absorbs the gap.
 std::vector<int64_t> plan_separators(int64_t N, int64_t rho) {
-  std::vector<int64_t> s;
   const int64_t step = rho + 1;
-  for (int64_t i = 0; i < N; i += step) s.push_back(i);
+  std::vector<int64_t> s((size_t)((N + step - 1) / step));
+  for (size_t k = 0; k < s.size(); ++k) s[k] = (int64_t)k * step;
+  s.reserve(s.size() + 1);
   if (s.back() != N - 1) {
     if (s.back() == N - 2) s.pop_back();
     s.push_back(N - 1);
@@ -640,11 +647,18 @@ static int create_impl(int64_t num_blocks, int64_t block_size, const btd_config*
     }
     LevelPlan lp;
     lp.N = cur;
-    lp.seps = plan_separators(cur, cfg->segment_length);
-    lp.P = (int64_t)lp.seps.size();
+    lp.step = cfg->segment_length + 1;
+    {  // separator count of plan_partition without materialising the list (bt/schur.py:75-95)
+      int64_t P0 = (cur + lp.step - 1) / lp.step;  // 0, step, 2 step, ... < cur
+      const int64_t last = (P0 - 1) * lp.step;
+      if (last != cur - 1) {
+        if (last == cur - 2) --P0;
+        ++P0;
+      }
+      lp.P = P0;
+    }
     lp.K = lp.P - 1;
-    int64_t maxlen = 0;
-    for (int64_t k = 0; k < lp.K; ++k) maxlen = std::max(maxlen, lp.seps[k + 1] - lp.seps[k] - 1);
+    const int64_t maxlen = lp.max_segment();
     if (maxlen > btd::kMaxBlockCoord) {
       delete h;
       set_status(st, BTD_ERR_UNSUPPORTED, "segment length %lld exceeds the device error-coordinate range",
@@ -725,7 +739,8 @@ int btd_level_info(const btd_hierarchy* h, int64_t level, int64_t* num_blocks, i
   const LevelPlan& lp = h->levels[level];
   if (num_blocks) *num_blocks = lp.N;
   if (num_separators) *num_separators = lp.P;
-  if (separators_out) std::copy(lp.seps.begin(), lp.seps.end(), separators_out);
+  if (separators_out)
+    for (int64_t k = 0; k < lp.P; ++k) separators_out[k] = lp.sep(k);
   return BTD_OK;
 }
 
@@ -764,7 +779,7 @@ cudaError_t chunked_level0(btd_hierarchy* h, btd::FactorArgs a, const LevelPlan&
     const int64_t ka = K * c / chunks, kb = K * (c + 1) / chunks;
     // segments [ka, kb) read diag/sub rows up to seps[kb] (exclusive for sub, inclusive for the
     // separator diag read by the assembly); the last chunk takes everything that is left
-    const int64_t row1 = (c + 1 == chunks) ? lp.N : lp.seps[kb] + 1;
+    const int64_t row1 = (c + 1 == chunks) ? lp.N : lp.sep(kb) + 1;
     e = cudaMemcpyAsync(src.dev_diag + row0 * nn, src.diag + row0 * nn, (size_t)(row1 - row0) * nn * sizeof(double),
                         cudaMemcpyHostToDevice, h->copy_stream);
     const int64_t srow1 = std::min<int64_t>(row1, lp.N - 1);
@@ -838,7 +853,7 @@ static int factorize_impl(btd_hierarchy* h, const double* diag, const double* su
     for (size_t l = 0; l < h->levels.size(); ++l) {
       LevelPlan& lp = h->levels[l];
       int jmax = 0;
-      for (int64_t kk = 0; kk < lp.K; ++kk) jmax = std::max<int>(jmax, (int)(lp.seps[kk + 1] - lp.seps[kk] - 1));
+      jmax = (int)lp.max_segment();
       BigCtx c{(const int*)(pers + lp.off_seps), lp.N, 0, (int)lp.K, err, stream};
       double* next_diag = (double*)(scr + lp.off_next_diag);
       prof_mark(h, stream);
@@ -1037,7 +1052,7 @@ static int solve_impl(const btd_hierarchy* h, const double* rhs, double* x, int6
     for (size_t l = 0; l < L && phase != kPhaseUp; ++l) {
       const LevelPlan& lp = h->levels[l];
       int jmax = 0;
-      for (int64_t kk = 0; kk < lp.K; ++kk) jmax = std::max<int>(jmax, (int)(lp.seps[kk + 1] - lp.seps[kk] - 1));
+      jmax = (int)lp.max_segment();
       const int* sp = (const int*)(pers + lp.off_seps);
       BigCtx c{sp, lp.N, 0, (int)lp.K, err, stream};
       e = big_solve_level(c, btd::kSolveDown, jmax, n, dd, rhs_l[l], (const double*)(pers + lp.off_linv),
@@ -1064,7 +1079,7 @@ static int solve_impl(const btd_hierarchy* h, const double* rhs, double* x, int6
     for (size_t l = L; l-- > 0;) {
       const LevelPlan& lp = h->levels[l];
       int jmax = 0;
-      for (int64_t kk = 0; kk < lp.K; ++kk) jmax = std::max<int>(jmax, (int)(lp.seps[kk + 1] - lp.seps[kk] - 1));
+      jmax = (int)lp.max_segment();
       const int* sp = (const int*)(pers + lp.off_seps);
       BigCtx c{sp, lp.N, 0, (int)lp.K, err, stream};
       const long long nn = (long long)n * n, ps = (long long)n * dd;
@@ -1086,7 +1101,7 @@ static int solve_impl(const btd_hierarchy* h, const double* rhs, double* x, int6
         e = big_copy(c, 0, btd::kActAll, opnd(x_l[l + 1], ps, dd, btd::kIdxSeg), opnd(x_l[l], ps, dd, btd::kIdxSegStart),
                      n, dd);
       if (e == cudaSuccess)
-        e = cudaMemcpyAsync(x_l[l] + (size_t)lp.seps[lp.K] * ps, x_l[l + 1] + (size_t)lp.K * ps, (size_t)pb,
+        e = cudaMemcpyAsync(x_l[l] + (size_t)lp.sep(lp.K) * ps, x_l[l + 1] + (size_t)lp.K * ps, (size_t)pb,
                             cudaMemcpyDeviceToDevice, stream);
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(big up)");
     }

@@ -308,8 +308,10 @@ __device__ int potrf_trtri(double* DL, int* s_fail, unsigned long long* leaf_bar
                                    : panel_chain<NT, false, BTD_RCP_CHAIN>(DL, p0, lane);
       if (lane == 0) *s_fail = f;
     } else if (p > 0) {
-      // helpers: leaf of panel p-1, and panel p-1's update of the column blocks >= p+1
-      if (warp == 1 + (p - 1) % (NWA > 1 ? NWA - 1 : 1)) {
+      // helpers: leaf of panel p-1 (warp 1), and panel p-1's update of the column blocks >= p+1
+      // (warps 2.. when there are at least two more helpers: the leaf is as long as a few tiles)
+      constexpr int T0 = NWA >= 3 ? 2 : 1;
+      if (warp == 1) {
         leaf_inverse<NT>(DL, p0 - 8, lane);
         if (leaf_bars) {  // publish leaf p-1 (streaming consumers, btd_factor3.cuh)
           __syncwarp();
@@ -319,7 +321,7 @@ __device__ int potrf_trtri(double* DL, int* s_fail, unsigned long long* leaf_bar
           }
         }
       }
-      tile_update_tri<NT, 4>(DL, p + 1, NP - p - 1, warp - 1, NWA - 1, p0 - 8, lane);
+      if (warp >= T0) tile_update_tri<NT, 4>(DL, p + 1, NP - p - 1, warp - T0, NWA - T0, p0 - 8, lane);
     }
     named_sync(kBarA, NWA * 32);
     BTD_PHASE(4);

@@ -45,11 +45,23 @@ class FactorLevel:
     ``plan`` is materialised lazily (a 2^20-block level has ~10^5 separators; building the
     Python tuples eagerly would dominate the host time of a factorization)."""
 
-    def __init__(self, num_blocks: int, separators: np.ndarray, level: int):
+    def __init__(self, num_blocks: int, num_separators: int, level: int, native):
         self.num_blocks = num_blocks
-        self.separators = separators
+        self.num_separators = num_separators
         self.level = level
+        self._native = native  # keeps the C handle alive for the lazy separator fetch
+        self._seps = None
         self._plan = None
+
+    @property
+    def separators(self) -> np.ndarray:
+        """Separator block indices of this level (fetched from the C plan on first use)."""
+        if self._seps is None:
+            seps = np.empty(self.num_separators, dtype=np.int64)
+            _native.lib().btd_level_info(self._native.handle, self.level, None, None,
+                                         seps.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+            self._seps = seps
+        return self._seps
 
     @property
     def plan(self) -> PartitionPlan:
@@ -58,7 +70,7 @@ class FactorLevel:
         return self._plan
 
     def __repr__(self):
-        return f"FactorLevel(level={self.level}, num_blocks={self.num_blocks}, separators={len(self.separators)})"
+        return f"FactorLevel(level={self.level}, num_blocks={self.num_blocks}, separators={self.num_separators})"
 
 
 @dataclass
@@ -212,9 +224,7 @@ def recursive_factorize(matrix: BlockTridiagonalMatrix, config: RecursionConfig 
     for lvl in range(nl.value):
         lnb, lp = ctypes.c_int64(), ctypes.c_int64()
         L.btd_level_info(handle, lvl, ctypes.byref(lnb), ctypes.byref(lp), None)
-        seps = np.empty(lp.value, dtype=np.int64)
-        L.btd_level_info(handle, lvl, None, None, seps.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
-        levels.append(FactorLevel(lnb.value, seps, lvl))
+        levels.append(FactorLevel(lnb.value, lp.value, lvl, native))
     return FactorHierarchy(N, n, levels, BaseFactor(nb.value, n), native)
 
 
