@@ -307,6 +307,7 @@ __device__ int potrf_trtri(double* DL, int* s_fail, unsigned long long* leaf_bar
       const int f = (p0 + 32 < NT) ? panel_chain<NT, true, BTD_RCP_CHAIN>(DL, p0, lane)
                                    : panel_chain<NT, false, BTD_RCP_CHAIN>(DL, p0, lane);
       if (lane == 0) *s_fail = f;
+      BTD_PHASE(6);
     } else if (p > 0) {
       // helpers: leaf of panel p-1 (warp 1), and panel p-1's update of the column blocks >= p+1
       // (warps 2.. when there are at least two more helpers: the leaf is as long as a few tiles)

@@ -53,7 +53,7 @@ void run() {
 #ifdef BTD_PHASE_PROF
   unsigned long long ph[16]; cudaMemcpyFromSymbol(ph, g_phase_cycles, sizeof(ph));
   unsigned long long z[16] = {0}; cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
-  printf("per call: chain+helpers %llu critical-update %llu leaves %llu combine %llu\n", ph[4]/20, ph[5]/20, ph[9]/20, ph[10]/20);
+  printf("per call: chain %llu wait-helpers %llu critical-update %llu leaves %llu combine %llu\n", ph[6]/20, ph[4]/20, ph[5]/20, ph[9]/20, ph[10]/20);
 #endif
   printf("{\"NT\":%d,\"cycles\":%lld,\"fail\":%lld,\"err\":%.2e,\"cuda\":\"%s\"}\n", NT, cyc[0], cyc[1], err, cudaGetErrorString(e));
 }
