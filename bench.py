@@ -178,6 +178,8 @@ def run_reference(args, rank, world):
 # GPU arm
 # ------------------------------------------------------------------------------------------
 def kernel_name(n):
+    if n <= 8:
+        return "factor_small_kernel level 0 (8-lane group per segment, btd_small.cuh)"
     if n > 64:
         return "level-0 tiled factor (big_potrf_kernel + bt_gemm_kernel sequence, btd_big.cuh)"
     nt = 8 if n <= 8 else 16 if n <= 16 else 32 if n <= 32 else 64

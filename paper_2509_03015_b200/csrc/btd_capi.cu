@@ -766,7 +766,9 @@ cudaError_t chunked_level0(btd_hierarchy* h, btd::FactorArgs a, const LevelPlan&
   }
   const size_t nn = (size_t)h->n * h->n;
   const int64_t K = lp.K;
-  const int64_t chunks = std::min<int64_t>(K, 16);
+  // chunks of >= ~64 MB: below that the per-chunk copy/event/launch overhead outweighs the overlap
+  const int64_t bytes = (2 * lp.N - 1) * (int64_t)nn * (int64_t)sizeof(double);
+  const int64_t chunks = std::max<int64_t>(1, std::min<int64_t>({K, (int64_t)16, bytes >> 26}));
   // the copy stream must not overwrite buffers a previous factorization on `stream` still reads
   cudaEvent_t ready;
   cudaError_t e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
