@@ -115,6 +115,12 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
                : "memory");
 }
 
+// Bulk prefetch of a contiguous global range into L2 (cp.async.bulk.prefetch.L2, no completion
+// tracking): used to pull the next step's diagonal block into L2 while the Cholesky runs.
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes & ~15u) : "memory");
+}
+
 // Stage an n x n row-major global block into an NT x LD shared tile, zero-padding rows/cols >= n.
 template <int NT, int LD, int NTHREADS>
 __device__ __forceinline__ void stage_block_async(double* sm, const double* g, int n) {
