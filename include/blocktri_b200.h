@@ -157,6 +157,23 @@ int btd_residual_norms(const double* diag, const double* sub, int64_t num_blocks
                        const double* x, const double* b, int64_t num_columns, void* workspace, double* norms2,
                        void* stream, btd_status* st);
 
+/* Kalman MAP-smoothing normal equations (build_normal_equations, kalman.py:130-162): one device
+ * pass assembling diag (N,n,n), sub (N-1,n,n), rhs (N,n) from the model arrays (device pointers,
+ * reference layouts).  flags: BTD_KALMAN_DIAG_R (meas_cov is (N,m) variances, else (N,m,m)),
+ * BTD_KALMAN_SHARED_{H,Q,R} (the array is one block shared by every step).  n <= 64; dense R:
+ * m <= 64.  A failing covariance returns BTD_ERR_NOT_POSITIVE_DEFINITE with pivot, block = step,
+ * member = 0 (process) / 1 (measurement).  workspace: btd_kalman_workspace() bytes. */
+#define BTD_KALMAN_DIAG_R 1
+#define BTD_KALMAN_SHARED_H 2
+#define BTD_KALMAN_SHARED_Q 4
+#define BTD_KALMAN_SHARED_R 8
+int btd_kalman_workspace(int64_t horizon, int64_t state_dim, size_t* bytes);
+int btd_kalman_normal_equations(int64_t horizon, int64_t state_dim, int64_t obs_dim, const double* transition,
+                                const double* observation, const double* process_cov, const double* meas_cov,
+                                const double* observations, const double* prior_offsets, int32_t flags,
+                                double* diag, double* sub, double* rhs, void* workspace, void* stream,
+                                btd_status* st);
+
 /* Process-wide count of kernels this library has launched (evidence for bench.py gpu_launches). */
 long long btd_launch_count(void);
 

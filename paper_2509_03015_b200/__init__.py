@@ -13,10 +13,12 @@ from .schur import (FactorLevel, RecursionConfig, level_factor, plan_partition, 
                     recursive_solve)
 from .synthgen import generate_spd_btd
 from .report import residual_report, btd_matmul
+from .kalman import StateSpaceModel, build_normal_equations, generate_rotation_model
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "StateSpaceModel", "build_normal_equations", "generate_rotation_model",
     "AsymmetricBlock", "BlockRhs", "BlockTriError", "BlockTridiagonalMatrix", "DeviceError",
     "DimensionMismatch", "FactorHierarchy", "FactorLevel", "InvalidDimensions", "LevelOverflow",
     "NotPositiveDefinite", "PartitionPlan", "RecursionConfig", "SingularDiagonal", "btd_matmul",

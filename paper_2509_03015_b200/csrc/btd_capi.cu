@@ -20,6 +20,7 @@
 #include "btd_big.cuh"
 #include "btd_spmv.cuh"
 #include "btd_small.cuh"
+#include "btd_kalman.cuh"
 
 namespace {
 
@@ -1333,6 +1334,83 @@ int btd_residual_norms(const double* diag, const double* sub, int64_t N, int64_t
   btd::btd_norm_finish_kernel<<<(unsigned)((2 * d + 127) / 128), 128, 0, s>>>(a.partial, (int)ctas, (int)d, norms2); g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(st, e, "btd_residual_norms");
+  return BTD_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Kalman normal equations (btd_kalman.cuh): build_normal_equations, bt/kalman.py:130-162.
+// ---------------------------------------------------------------------------------------------
+int btd_kalman_workspace(int64_t horizon, int64_t state_dim, size_t* bytes) {
+  if (horizon < 1 || state_dim < 1 || !bytes) return BTD_ERR_INVALID_ARGUMENT;
+  *bytes = align_up((size_t)horizon * state_dim * state_dim * sizeof(double)) + kAlign;
+  return BTD_OK;
+}
+
+int btd_kalman_normal_equations(int64_t horizon, int64_t n, int64_t m, const double* transition,
+                                const double* observation, const double* process_cov, const double* meas_cov,
+                                const double* observations, const double* prior_offsets, int32_t flags,
+                                double* diag, double* sub, double* rhs, void* workspace, void* stream,
+                                btd_status* st) {
+  clear_status(st);
+  const bool diag_r = flags & BTD_KALMAN_DIAG_R;
+  if (horizon < 1 || n < 1 || m < 1 || !transition || !observation || !process_cov || !meas_cov ||
+      !observations || !prior_offsets || !diag || !rhs || !workspace || (horizon > 1 && !sub)) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_kalman_normal_equations: bad arguments");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  if (n > btd::kKalmanMaxN || (!diag_r && m > btd::kKalmanMaxDenseM)) {
+    set_status(st, BTD_ERR_UNSUPPORTED, "Kalman assembly kernel: state_dim <= %d and (dense R) obs_dim <= %d",
+               btd::kKalmanMaxN, btd::kKalmanMaxDenseM);
+    return BTD_ERR_UNSUPPORTED;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  char* ws = (char*)workspace;
+  unsigned long long* err = (unsigned long long*)ws;
+  double* cross = (double*)(ws + kAlign);
+  btd::KalmanArgs a{};
+  a.transition = transition;
+  a.observation = observation;
+  a.process_cov = process_cov;
+  a.meas_cov = meas_cov;
+  a.observations = observations;
+  a.prior = prior_offsets;
+  a.N = horizon;
+  a.n = (int)n;
+  a.m = (int)m;
+  a.diag_r = diag_r ? 1 : 0;
+  a.shared_h = (flags & BTD_KALMAN_SHARED_H) ? 1 : 0;
+  a.shared_q = (flags & BTD_KALMAN_SHARED_Q) ? 1 : 0;
+  a.shared_r = (flags & BTD_KALMAN_SHARED_R) ? 1 : 0;
+  a.diag = diag;
+  a.sub = sub;
+  a.rhs = rhs;
+  a.cross = cross;
+  a.err = err;
+  const size_t smem = btd::kalman_smem_doubles((int)n, (int)m, diag_r ? 0 : 1) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(btd::kalman_terms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return cuda_fail(st, e, "btd_kalman_normal_equations(attr)");
+  e = cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return cuda_fail(st, e, "btd_kalman_normal_equations(init)");
+  btd::kalman_terms_kernel<<<(unsigned)horizon, btd::kKalmanThreads, smem, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
+  btd::kalman_finish_kernel<<<flat_grid(horizon * n * n), 256, 0, s>>>(diag, cross, horizon, (int)n, err); g_launches.fetch_add(1, std::memory_order_relaxed);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(st, e, "btd_kalman_normal_equations(launch)");
+  unsigned long long key = 0;
+  e = cudaMemcpyAsync(&key, err, sizeof(key), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(st, e, "btd_kalman_normal_equations(sync)");
+  if (key != btd::kNoErr) {
+    const long long k = (long long)(key >> 20);
+    const int kind = (int)((key >> 16) & 0xf), pivot = (int)(key & 0xffff);
+    set_status(st, BTD_ERR_NOT_POSITIVE_DEFINITE, "%s covariance is not positive definite at pivot %d, step %lld",
+               kind == 0 ? "process" : "measurement", pivot, k);
+    st->pivot = pivot;
+    st->block = k;
+    st->member = kind;  // 0: process covariance, 1: measurement covariance
+    st->level = -1;
+    return BTD_ERR_NOT_POSITIVE_DEFINITE;
+  }
   return BTD_OK;
 }
 
