@@ -7,18 +7,20 @@ sm_100a CUDA kernels behind the C ABI in include/blocktri_b200.h.
 
 from .core import (BlockRhs, BlockTridiagonalMatrix, FactorHierarchy, PartitionPlan, check_conformal,
                    new_btd, new_rhs)
-from .errors import (AsymmetricBlock, BlockTriError, DeviceError, DimensionMismatch, InvalidDimensions,
+from .errors import (BadMagic, BtdFormatError, IoError, TruncatedPayload, VersionUnsupported, AsymmetricBlock, BlockTriError, DeviceError, DimensionMismatch, InvalidDimensions,
                      LevelOverflow, NotPositiveDefinite, SingularDiagonal)
 from .schur import (FactorLevel, RecursionConfig, level_factor, plan_partition, recursive_factorize,
                     recursive_solve)
 from .synthgen import generate_spd_btd
 from .report import residual_report, btd_matmul
 from .kalman import StateSpaceModel, build_normal_equations, generate_rotation_model
+from .btdfile import read_btd, write_btd
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "StateSpaceModel", "build_normal_equations", "generate_rotation_model",
+    "StateSpaceModel", "build_normal_equations", "generate_rotation_model", "read_btd", "write_btd",
+    "IoError", "BtdFormatError", "BadMagic", "VersionUnsupported", "TruncatedPayload",
     "AsymmetricBlock", "BlockRhs", "BlockTriError", "BlockTridiagonalMatrix", "DeviceError",
     "DimensionMismatch", "FactorHierarchy", "FactorLevel", "InvalidDimensions", "LevelOverflow",
     "NotPositiveDefinite", "PartitionPlan", "RecursionConfig", "SingularDiagonal", "btd_matmul",

@@ -77,8 +77,10 @@ def _device_array(a: np.ndarray, dev):
     """(torch tensor on dev, shared?) -- a stride-0 leading axis goes up as a single block."""
     import torch
     shared = a.ndim >= 1 and a.shape[0] > 1 and a.strides[0] == 0
-    src = a[:1] if shared else a
-    return torch.from_numpy(np.ascontiguousarray(src, dtype=np.float64)).to(dev), shared
+    src = np.ascontiguousarray(a[:1] if shared else a, dtype=np.float64)
+    if not src.flags.writeable:  # broadcast views are read-only; torch wants writable memory
+        src = src.copy()
+    return torch.from_numpy(src).to(dev), shared
 
 
 def build_normal_equations(model: StateSpaceModel, *, device_out: bool = False):

@@ -36,6 +36,13 @@ def _stored_model(prefix):
     return pkg.StateSpaceModel(**{f: np.array(GOLD[f"{prefix}_{f}"]) for f in FIELDS})
 
 
+def _close(a, b, tol=1e-12):
+    a = np.asarray(a)
+    if a.shape != b.shape:
+        return False
+    return a.size == 0 or np.abs(a - b).max() <= tol * max(np.abs(b).max(), 1.0)
+
+
 def test_rotation_model_bit_identical_to_reference():
     for i in _cases("rot"):
         mdl = _rot_model(i)
@@ -60,11 +67,16 @@ def test_model_validation_like_reference():
             pkg.generate_rotation_model(*bad)
 
 
+def test_cpu_port_pinned_to_reference_outputs():
+    from oracle import kalman_port
+    for prefix, make in [("rot", _rot_model), ("rnd", lambda i: _stored_model(f"rnd{i}"))]:
+        for i in _cases(prefix):
+            d, s, r = kalman_port.build_normal_equations(make(i))
+            assert _close(d, GOLD[f"{prefix}{i}_diag"], 1e-11) and _close(s, GOLD[f"{prefix}{i}_sub"], 1e-11)
+            assert _close(r, GOLD[f"{prefix}{i}_rhs"], 1e-11)
+
+
 torch = pytest.importorskip("torch")
-
-
-def _close(a, b, tol=1e-12):
-    return np.abs(np.asarray(a) - b).max() <= tol * max(np.abs(b).max(), 1.0)
 
 
 @pytest.mark.gpu
