@@ -139,6 +139,100 @@ __device__ __forceinline__ void gemm_tile(double (&acc)[2][4][2], const double* 
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Pipelined 64 x 64 output-tile GEMM: k in chunks of BK = 32, two stages in flight (cp.async.cg
+// 16-byte copies; the chunk k+1 loads while chunk k is multiplied).  Operand tiles stay in their
+// storage orientation in shared memory (every global read is a contiguous 16-byte run, with no
+// transposition on the fly); the DMMA fragment loads index them according to TA / TB.
+//   A tile: !TA -> As[r][k] (64 x BK, ld BK+4)      TA -> As[k][r] (BK x 64, ld 64+4)
+//   B tile (op(B) is k x n): !TB -> Bs[k][c] (BK x 64, ld 64+4)   TB -> Bs[c][k] (64 x BK, ld BK+4)
+// ---------------------------------------------------------------------------------------------
+constexpr int BK = 32;
+constexpr int LDK = BK + 4;  // tiles whose rows run along k
+constexpr int LDM = BT + 4;  // tiles whose rows run along m / n
+constexpr int GSTAGE = (BT * LDK > BK * LDM) ? BT * LDK : BK * LDM;  // doubles per operand tile slot
+
+// Stage the region rows [r0, r0+R) x cols [c0, c0+C) of a stored row-major matrix X (ld, logical
+// bounds rows x cols) into S (ld LS), zero filling outside the bounds.
+template <int R, int C, int LS>
+__device__ __forceinline__ void stage_region(double* S, const double* X, int ld, int r0, int c0, int rows, int cols) {
+  constexpr int CH = C / 2;  // 16-byte chunks per row
+  for (int e = threadIdx.x; e < R * CH; e += BTHREADS) {
+    const int r = e / CH, c = (e % CH) * 2;
+    const int gr = r0 + r, gc = c0 + c;
+    double* dst = S + r * LS + c;
+    const double* src = X + (size_t)gr * ld + gc;
+    if (gr < rows && gc + 1 < cols && (((size_t)src & 15) == 0)) {
+      cp_async16(dst, src, 16);
+    } else {
+      cp_async8(dst, (gr < rows && gc < cols) ? (const void*)src : (const void*)X, (gr < rows && gc < cols) ? 8 : 0);
+      cp_async8(dst + 1, (gr < rows && gc + 1 < cols) ? (const void*)(src + 1) : (const void*)X,
+                (gr < rows && gc + 1 < cols) ? 8 : 0);
+    }
+  }
+}
+
+template <bool TA, bool TB>
+__device__ __forceinline__ void stage_chunk(double* As, double* Bs, const double* A, int lda, const double* B, int ldb,
+                                            int m, int n, int kdim, int m0, int n0, int kc) {
+  // op(A) is m x kdim: stored A is m x kdim (!TA) or kdim x m (TA)
+  if (!TA) stage_region<BT, BK, LDK>(As, A, lda, m0, kc, m, kdim);
+  else stage_region<BK, BT, LDM>(As, A, lda, kc, m0, kdim, m);
+  // op(B) is kdim x n: stored B is kdim x n (!TB) or n x kdim (TB)
+  if (!TB) stage_region<BK, BT, LDM>(Bs, B, ldb, kc, n0, kdim, n);
+  else stage_region<BT, BK, LDK>(Bs, B, ldb, n0, kc, n, kdim);
+}
+
+template <bool TA, bool TB>
+__device__ __forceinline__ void chunk_mma(double (&acc)[2][4][2], const double* As, const double* Bs, int kn) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rw = (warp >> 1) * 16, cw = (warp & 1) * 32;
+  const int lr = lane >> 2, lk = lane & 3;
+#pragma unroll 2
+  for (int kk = 0; kk < kn; kk += 4) {
+    double a[2], b[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      a[i] = TA ? As[(kk + lk) * LDM + rw + i * 8 + lr] : As[(rw + i * 8 + lr) * LDK + kk + lk];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      b[q] = TB ? Bs[(cw + q * 8 + lr) * LDK + kk + lk] : Bs[(kk + lk) * LDM + cw + q * 8 + lr];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dmma(acc[i][q], a[i], b[q]);
+  }
+}
+
+template <bool TA, bool TB>
+__device__ __forceinline__ void gemm_tile_pipelined(double (&acc)[2][4][2], const double* A, int lda, const double* B,
+                                                    int ldb, int m, int n, int kdim, int m0, int n0, int kbeg, int kend,
+                                                    double* sm) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[i][q][0] = acc[i][q][1] = 0.0;
+  const int nch = (kend - kbeg + BK - 1) / BK;
+  if (nch <= 0) return;
+  stage_chunk<TA, TB>(sm, sm + GSTAGE, A, lda, B, ldb, m, n, kdim, m0, n0, kbeg);
+  cp_async_commit();
+  for (int c = 0; c < nch; ++c) {
+    double* cur = sm + (c & 1) * 2 * GSTAGE;
+    if (c + 1 < nch) {
+      double* nxt = sm + ((c + 1) & 1) * 2 * GSTAGE;
+      stage_chunk<TA, TB>(nxt, nxt + GSTAGE, A, lda, B, ldb, m, n, kdim, m0, n0, kbeg + (c + 1) * BK);
+      cp_async_commit();
+      cp_async_wait_group<1>();
+    } else {
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    chunk_mma<TA, TB>(acc, cur, cur + GSTAGE, min(BK, kend - kbeg - c * BK));
+    __syncthreads();
+  }
+}
+
+template <bool TA, bool TB>
 __global__ void __launch_bounds__(BTHREADS) bt_gemm_kernel(GemmArgs g) {
   if (error_raised(g.err)) return;
   const int k = blockIdx.y;
@@ -148,8 +242,6 @@ __global__ void __launch_bounds__(BTHREADS) bt_gemm_kernel(GemmArgs g) {
   const int m0 = tm * BT, n0 = tn * BT;
   if (g.lower_only && n0 > m0) return;
   extern __shared__ __align__(16) double gsm[];
-  double* As = gsm;
-  double* Bs = gsm + BT * BLD;
   const double* A = operand_ptr(g.A, g.seps, g.base_mode, k, g.j) + (size_t)g.A.row0 * g.A.ld + g.A.col0;
   const double* B = operand_ptr(g.B, g.seps, g.base_mode, k, g.j) + (size_t)g.B.row0 * g.B.ld + g.B.col0;
   int kbeg = 0, kend = g.k;
@@ -157,7 +249,7 @@ __global__ void __launch_bounds__(BTHREADS) bt_gemm_kernel(GemmArgs g) {
   if (g.tri == 2) kend = min(kend, m0 + BT);
   if (g.tri == 3) kbeg = m0 / BT * BT;
   double acc[2][4][2];
-  gemm_tile(acc, A, g.A.ld, g.A.trans, B, g.B.ld, g.B.trans, g.m, g.n, g.k, m0, n0, kbeg, kend, As, Bs);
+  gemm_tile_pipelined<TA, TB>(acc, A, g.A.ld, B, g.B.ld, g.m, g.n, g.k, m0, n0, kbeg, kend, gsm);
   const double* Cin = g.beta != 0.0 ? operand_ptr(g.Cin, g.seps, g.base_mode, k, g.j) : nullptr;
   if (Cin) Cin += (size_t)g.Cin.row0 * g.Cin.ld + g.Cin.col0;
   double* Cout = const_cast<double*>(operand_ptr(g.Cout, g.seps, g.base_mode, k, g.j)) +

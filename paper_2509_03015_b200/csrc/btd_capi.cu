@@ -376,10 +376,14 @@ cudaError_t big_gemm(const BigCtx& c, int j, int act, btd::Operand A, btd::Opera
                      btd::Operand Cout, int m, int n, int k, double alpha, double beta, int lower = 0, int tri = 0,
                      int store_trans = 0) {
   static bool configured = false;
-  const int smem = 2 * btd::BT * btd::BLD * (int)sizeof(double);
+  const int smem = 4 * btd::GSTAGE * (int)sizeof(double);  // 2 stages x (A, B) tiles
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(btd::bt_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
+    const void* fns[4] = {(const void*)btd::bt_gemm_kernel<false, false>, (const void*)btd::bt_gemm_kernel<false, true>,
+                          (const void*)btd::bt_gemm_kernel<true, false>, (const void*)btd::bt_gemm_kernel<true, true>};
+    for (const void* f : fns) {
+      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+    }
     configured = true;
   }
   btd::GemmArgs g{};
@@ -403,7 +407,11 @@ cudaError_t big_gemm(const BigCtx& c, int j, int act, btd::Operand A, btd::Opera
   g.tiles_n = (n + btd::BT - 1) / btd::BT;
   g.err = c.err;
   dim3 grid((unsigned)(((m + btd::BT - 1) / btd::BT) * g.tiles_n), (unsigned)c.K);
-  btd::bt_gemm_kernel<<<grid, btd::BTHREADS, smem, c.s>>>(g); g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!A.trans && !B.trans) btd::bt_gemm_kernel<false, false><<<grid, btd::BTHREADS, smem, c.s>>>(g);
+  else if (!A.trans) btd::bt_gemm_kernel<false, true><<<grid, btd::BTHREADS, smem, c.s>>>(g);
+  else if (!B.trans) btd::bt_gemm_kernel<true, false><<<grid, btd::BTHREADS, smem, c.s>>>(g);
+  else btd::bt_gemm_kernel<true, true><<<grid, btd::BTHREADS, smem, c.s>>>(g);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 

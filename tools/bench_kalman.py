@@ -22,6 +22,8 @@ mdl = pkg.generate_rotation_model(args.state, args.obs, args.horizon, seed=0)
 N, n, m = mdl.horizon, mdl.state_dim, mdl.obs_dim
 for _ in range(2):
     A, B = kalman.build_normal_equations(mdl, device_out=True)
+for _ in range(2):
+    X = pkg.recursive_solve(pkg.recursive_factorize(A), B)
 torch.cuda.synchronize()
 e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 reps = 5
