@@ -77,68 +77,6 @@ struct GemmArgs {
   const DevErr* err;
 };
 
-// Stage the 64 x 64 tile of op(X) at (r0, c0) (op-matrix coordinates, rows x cols bounded) into
-// shared memory S[r][c] (leading dimension BLD) with zero fill.
-__device__ __forceinline__ void stage_op_tile(double* S, const double* X, int ld, int trans, int r0, int c0,
-                                              int rows, int cols) {
-  for (int e = threadIdx.x; e < BT * BT; e += BTHREADS) {
-    int r, c;
-    if (!trans) {
-      r = e / BT, c = e % BT;  // coalesced along c
-    } else {
-      c = e / BT, r = e % BT;  // coalesced along r (stored row c0 + c)
-    }
-    const int gr = r0 + r, gc = c0 + c;
-    double* dst = S + r * BLD + c;
-    if (gr < rows && gc < cols) {
-      const double* src = trans ? X + (size_t)gc * ld + gr : X + (size_t)gr * ld + gc;
-      cp_async8(dst, src, 8);
-    } else {
-      *dst = 0.0;
-    }
-  }
-}
-
-// acc (warp tile 16 x 32) += As(64 x 64) * Bs(64 x 64)^T restricted to k in [k0, k1)
-__device__ __forceinline__ void tile_mma(double (&acc)[2][4][2], const double* As, const double* Bs, int k0, int k1) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int rw = (warp >> 1) * 16, cw = (warp & 1) * 32;
-  const double* pa = As + (rw + (lane >> 2)) * BLD + (lane & 3);
-  const double* pb = Bs + (cw + (lane >> 2)) * BLD + (lane & 3);
-  for (int kk = k0; kk < k1; kk += 4) {
-    double a[2], b[4];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) a[i] = pa[i * 8 * BLD + kk];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) b[q] = pb[q * 8 * BLD + kk];
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) dmma(acc[i][q], a[i], b[q]);
-  }
-}
-
-// One 64 x 64 output tile at (m0, n0) of alpha op(A) op(B) (+ beta Cin): the k loop runs over
-// 64-wide chunks staged through two shared tiles (A chunk, B^T chunk).
-__device__ __forceinline__ void gemm_tile(double (&acc)[2][4][2], const double* A, int lda, int ta, const double* B,
-                                          int ldb, int tb, int m, int n, int kdim, int m0, int n0, int kbeg, int kend,
-                                          double* As, double* Bs) {
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[i][q][0] = acc[i][q][1] = 0.0;
-  for (int kc = kbeg; kc < kend; kc += BT) {
-    __syncthreads();
-    stage_op_tile(As, A, lda, ta, m0, kc, m, kdim);
-    // op(B) is kdim x n; we need Bs[c][k] = op(B)[kc + k][n0 + c] = op(B)^T tile
-    stage_op_tile(Bs, B, ldb, !tb, n0, kc, n, kdim);
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncthreads();
-    tile_mma(acc, As, Bs, 0, min(BT, kend - kc));
-  }
-}
-
 // ---------------------------------------------------------------------------------------------
 // Pipelined 64 x 64 output-tile GEMM: k in chunks of BK = 32, two stages in flight (cp.async.cg
 // 16-byte copies; the chunk k+1 loads while chunk k is multiplied).  Operand tiles stay in their
@@ -319,8 +257,7 @@ __global__ void __launch_bounds__(BTHREADS) big_potrf_kernel(BigPotrfArgs g) {
   if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, kActAll, J)) return;
   extern __shared__ __align__(16) double sm[];
   double* DL = sm;             // 64 x LD diagonal tile
-  double* As = DL + BT * LD;   // staging tiles for the tile GEMMs
-  double* Bs = As + BT * BLD;
+  double* As = DL + BT * LD;   // two-stage staging of the tile GEMMs (4 * GSTAGE doubles)
   __shared__ int s_fail;
   double* D = const_cast<double*>(operand_ptr(g.D, g.seps, g.base_mode, k, g.j));
   double* Li = const_cast<double*>(operand_ptr(g.Linv, g.seps, g.base_mode, k, g.j));
@@ -360,8 +297,7 @@ __global__ void __launch_bounds__(BTHREADS) big_potrf_kernel(BigPotrfArgs g) {
     }
     // panel: L_ib = A_ib Linv_kk^T  (i > kb), in place in D
     for (int ib = kb + 1; ib < NB; ++ib) {
-      gemm_tile(acc, D + (size_t)ib * BT * n + kb * BT, n, 0, Li + (size_t)kb * BT * n + kb * BT, n, 1, BT, BT, BT,
-                0, 0, 0, BT, As, Bs);
+      gemm_tile_pipelined<false, true>(acc, D + (size_t)ib * BT * n + kb * BT, n, Li + (size_t)kb * BT * n + kb * BT, n, BT, BT, BT, 0, 0, 0, BT, As);
       __syncthreads();
       store_acc(D + (size_t)ib * BT * n + kb * BT, n, acc, 1.0, nullptr);
     }
@@ -369,8 +305,7 @@ __global__ void __launch_bounds__(BTHREADS) big_potrf_kernel(BigPotrfArgs g) {
     // trailing: A_ij -= L_ib L_jb^T  (kb < jb <= ib)
     for (int ib = kb + 1; ib < NB; ++ib)
       for (int jb = kb + 1; jb <= ib; ++jb) {
-        gemm_tile(acc, D + (size_t)ib * BT * n + kb * BT, n, 0, D + (size_t)jb * BT * n + kb * BT, n, 1, BT, BT, BT,
-                  0, 0, 0, BT, As, Bs);
+        gemm_tile_pipelined<false, true>(acc, D + (size_t)ib * BT * n + kb * BT, n, D + (size_t)jb * BT * n + kb * BT, n, BT, BT, BT, 0, 0, 0, BT, As);
         __syncthreads();
         double* t = D + (size_t)ib * BT * n + jb * BT;
         store_acc(t, n, acc, -1.0, t);
@@ -382,15 +317,13 @@ __global__ void __launch_bounds__(BTHREADS) big_potrf_kernel(BigPotrfArgs g) {
   for (int ib = 1; ib < NB; ++ib) {
     for (int jb = 0; jb < ib; ++jb) {
       // T = L[ib][jb..ib-1] * Linv[jb..ib-1][jb]   (k range (ib - jb) tiles)
-      gemm_tile(acc, D + (size_t)ib * BT * n + jb * BT, n, 0, Li + (size_t)jb * BT * n + jb * BT, n, 0, BT, BT,
-                (ib - jb) * BT, 0, 0, 0, (ib - jb) * BT, As, Bs);
+      gemm_tile_pipelined<false, false>(acc, D + (size_t)ib * BT * n + jb * BT, n, Li + (size_t)jb * BT * n + jb * BT, n, BT, BT, (ib - jb) * BT, 0, 0, 0, (ib - jb) * BT, As);
       __syncthreads();
       store_acc(D + (size_t)jb * BT * n + ib * BT, n, acc, 1.0, nullptr);
     }
     __syncthreads();
     for (int jb = 0; jb < ib; ++jb) {
-      gemm_tile(acc, Li + (size_t)ib * BT * n + ib * BT, n, 0, D + (size_t)jb * BT * n + ib * BT, n, 0, BT, BT, BT, 0,
-                0, 0, BT, As, Bs);
+      gemm_tile_pipelined<false, false>(acc, Li + (size_t)ib * BT * n + ib * BT, n, D + (size_t)jb * BT * n + ib * BT, n, BT, BT, BT, 0, 0, 0, BT, As);
       __syncthreads();
       store_acc(Li + (size_t)ib * BT * n + jb * BT, n, acc, -1.0, nullptr);
     }

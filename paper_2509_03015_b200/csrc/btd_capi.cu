@@ -475,7 +475,7 @@ cudaError_t big_factor_level(const BigCtx& c, int level, int Jmax, int n, const 
       a.n = n;
       a.level = level;
       a.err = err;
-      const int smem = 3 * BT * FactorShape<64>::LD * (int)sizeof(double);
+      const int smem = (BT * FactorShape<64>::LD + 4 * GSTAGE) * (int)sizeof(double);
       static bool conf = false;
       if (!conf) {
         BIG_CHECK(cudaFuncSetAttribute(big_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
