@@ -30,7 +30,7 @@ srcs = {}
 for (ln, (s, i)) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:45]:
     src = ''
     if ln:
-        fn = {'btd_factor.cuh': 'paper_2509_03015_b200/csrc/btd_factor.cuh', 'btd_solve.cuh': 'paper_2509_03015_b200/csrc/btd_solve.cuh', 'btd_device.cuh': 'paper_2509_03015_b200/csrc/btd_device.cuh'}.get(ln[0])
+        fn = {'btd_small.cuh': 'paper_2509_03015_b200/csrc/btd_small.cuh', 'btd_factor.cuh': 'paper_2509_03015_b200/csrc/btd_factor.cuh', 'btd_solve.cuh': 'paper_2509_03015_b200/csrc/btd_solve.cuh', 'btd_device.cuh': 'paper_2509_03015_b200/csrc/btd_device.cuh'}.get(ln[0])
         if fn:
             src = open(fn).read().splitlines()[ln[1] - 1].strip()[:70]
     print(f"{100*s/tot:5.1f}%  inst {i:11d}  {str(ln):32s} {src}")
