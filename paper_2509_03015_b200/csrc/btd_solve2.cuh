@@ -2,8 +2,8 @@
 //
 // Same algebra as btd_solve.cuh (down: w = A_uu^{-1} b_u, fold f_L = C_L^T w_0, f_R = C_R w_last;
 // up: b_0 -= C_L x_L, b_last -= C_R^T x_R, then forward/backward sweep), but built for HBM
-// bandwidth: every block the sweep needs is streamed global->shared through a STAGES-deep cp.async
-// ring that runs ahead of the arithmetic across segment boundaries, and the inverse diagonal
+// bandwidth: every block the sweep needs is streamed global->shared by a TMA producer warp through
+// an mbarrier ring that runs ahead of the arithmetic across segment boundaries, and the inverse diagonal
 // factors are read in packed lower-triangular form (n(n+1)/2 instead of n^2 doubles).  The
 // backward sweep re-reads a segment's blocks right after the forward sweep, so they come from L2.
 //
@@ -41,227 +41,6 @@ __host__ __device__ __forceinline__ int packed_row_offset(int r) {
 __host__ __device__ __forceinline__ int packed_stride(int n) { return packed_row_offset(n); }
 
 enum StepKind : int { kStepF = 0, kStepB = 1, kStepCL = 2, kStepCR = 3, kStepNone = 4 };
-
-struct StepDesc {
-  const double* full;  // n x n (Lsub or coupling block), or nullptr
-  const double* pack;  // packed Linv, or nullptr
-  const double* vec;   // n x d panel (rhs row or separator solution), or nullptr
-  int kind, j;
-};
-
-// Step `idx` of segment k.  Returns false past the end of the segment's stream.
-__device__ __forceinline__ bool make_step(const SolveArgs& a, int k, int idx, StepDesc& s, int& J_out) {
-  const long long start = (long long)a.seps[k] + 1, stop = (long long)a.seps[k + 1];
-  const int J = (int)(stop - start);
-  J_out = J;
-  const size_t bs = (size_t)a.n * a.n, ps = (size_t)a.n * a.d, pk = (size_t)packed_stride(a.n);
-  if (idx >= 2 * J + 2) return false;
-  s.full = s.pack = s.vec = nullptr;
-  int kind, j;
-  if (a.mode == kSolveDown) {
-    if (idx < J) {
-      kind = kStepF, j = idx;
-    } else if (idx == J) {
-      kind = kStepB, j = J - 1;
-    } else if (idx == J + 1) {
-      kind = kStepCR, j = J - 1;
-    } else if (idx < 2 * J + 1) {
-      kind = kStepB, j = J - 2 - (idx - J - 2);
-    } else {
-      kind = kStepCL, j = 0;
-    }
-  } else {  // up
-    if (idx == 0) {
-      kind = kStepCL, j = 0;
-    } else if (idx < J) {
-      kind = kStepF, j = idx - 1;  // F_0 .. F_{J-2}
-    } else if (idx == J) {
-      kind = kStepCR, j = J - 1;
-    } else if (idx == J + 1) {
-      kind = kStepF, j = J - 1;
-    } else {
-      kind = kStepB, j = J - 1 - (idx - J - 2);
-    }
-  }
-  const long long row = start + j;
-  if (kind == kStepF) {
-    s.pack = a.Linv + row * pk;
-    if (j > 0) s.full = a.Lsub + (row - 1) * bs;
-    s.vec = a.rhs + row * ps;
-  } else if (kind == kStepB) {
-    s.pack = a.Linv + row * pk;
-    if (j < J - 1) s.full = a.Lsub + row * bs;
-  } else if (kind == kStepCL) {
-    s.full = a.Lsub + (start - 1) * bs;
-    if (a.mode == kSolveUp) s.vec = a.xsep + (size_t)k * ps;
-  } else {
-    s.full = a.Lsub + (stop - 1) * bs;
-    if (a.mode == kSolveUp) s.vec = a.xsep + (size_t)(k + 1) * ps;
-  }
-  s.kind = kind;
-  s.j = j;
-  return true;
-}
-
-template <int NT, int DC>
-__device__ __forceinline__ void issue_stage(double* st, const StepDesc& s, int n, int d, int c0, int dc) {
-  using S = Solve2Shape<NT>;
-  const int tid = threadIdx.x;
-  double* sf = st;
-  double* sp = st + S::FULL;
-  double* sv = st + S::FULL + S::PACK;
-  const bool even = (n & 1) == 0;
-  if (s.full) {
-    if (even) {
-      for (int i = tid; i < n * n / 2; i += S::NTHREADS) cp_async16(sf + 2 * i, s.full + 2 * i, 16);
-    } else {
-      for (int i = tid; i < n * n; i += S::NTHREADS) cp_async8(sf + i, s.full + i, 8);
-    }
-  }
-  if (s.pack) {
-    const int np = packed_stride(n);
-    for (int i = tid; i < np / 2; i += S::NTHREADS) cp_async16(sp + 2 * i, s.pack + 2 * i, 16);
-  }
-  if (s.vec) {
-    for (int e = tid; e < n * DC; e += S::NTHREADS) {
-      const int r = e / DC, c = e % DC;
-      if (c < dc) cp_async8(sv + e, s.vec + (size_t)r * d + c0 + c, 8);
-    }
-  }
-}
-
-// y (+)= sign * M x   (M dense n x n, row stride n, in shared memory)
-template <int NT, int DC>
-__device__ __forceinline__ void mv_full(const double* M, const double* x, double* y, int n, double sign,
-                                        bool accumulate) {
-  using S = Solve2Shape<NT>;
-  const int tid = threadIdx.x, r = tid / S::PARTS, part = tid % S::PARTS;
-  double acc[DC];
-#pragma unroll
-  for (int c = 0; c < DC; ++c) acc[c] = 0.0;
-  if (r < n) {
-#pragma unroll 4
-    for (int i = 0; i < S::SPAN; ++i) {
-      const int m = part * S::SPAN + (i + r) % S::SPAN;  // rotated: conflict-free rows
-      if (m < n) {
-        const double v = M[r * n + m];
-#pragma unroll
-        for (int c = 0; c < DC; ++c) acc[c] = fma(v, x[m * DC + c], acc[c]);
-      }
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < DC; ++c) {
-    acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 1);
-    acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 2);
-  }
-  if (part == 0 && r < NT) {
-#pragma unroll
-    for (int c = 0; c < DC; ++c) {
-      const double v = r < n ? sign * acc[c] : 0.0;
-      y[r * DC + c] = accumulate ? y[r * DC + c] + v : v;
-    }
-  }
-}
-
-// y (+)= sign * M^T x   (dense), reduction over the 4 row slices through `red`
-template <int NT, int DC>
-__device__ __forceinline__ void mv_full_t(const double* M, const double* x, double* y, int n, double sign,
-                                          bool accumulate, double* red) {
-  using S = Solve2Shape<NT>;
-  const int tid = threadIdx.x, col = tid % NT, part = tid / NT;
-  double acc[DC];
-#pragma unroll
-  for (int c = 0; c < DC; ++c) acc[c] = 0.0;
-  if (col < n) {
-#pragma unroll 4
-    for (int i = 0; i < S::SPAN; ++i) {
-      const int m = part * S::SPAN + i;
-      if (m < n) {
-        const double v = M[m * n + col];
-#pragma unroll
-        for (int c = 0; c < DC; ++c) acc[c] = fma(v, x[m * DC + c], acc[c]);
-      }
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < DC; ++c) red[(part * NT + col) * DC + c] = acc[c];
-  __syncthreads();
-  if (part == 0) {
-#pragma unroll
-    for (int c = 0; c < DC; ++c) {
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < S::PARTS; ++q) s += red[(q * NT + col) * DC + c];
-      const double v = col < n ? sign * s : 0.0;
-      y[col * DC + c] = accumulate ? y[col * DC + c] + v : v;
-    }
-  }
-}
-
-// y = Lp x   (packed lower triangular: row r at r(r+1)/2)
-template <int NT, int DC>
-__device__ __forceinline__ void mv_pack(const double* P, const double* x, double* y, int n) {
-  using S = Solve2Shape<NT>;
-  const int tid = threadIdx.x, r = tid / S::PARTS, part = tid % S::PARTS;
-  double acc[DC];
-#pragma unroll
-  for (int c = 0; c < DC; ++c) acc[c] = 0.0;
-  if (r < n) {
-    const double* row = P + packed_row_offset(r);
-#pragma unroll 4
-    for (int i = 0; i < S::SPAN; ++i) {
-      const int m = part * S::SPAN + (i + r) % S::SPAN;
-      if (m <= r) {
-        const double v = row[m];
-#pragma unroll
-        for (int c = 0; c < DC; ++c) acc[c] = fma(v, x[m * DC + c], acc[c]);
-      }
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < DC; ++c) {
-    acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 1);
-    acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 2);
-  }
-  if (part == 0 && r < NT) {
-#pragma unroll
-    for (int c = 0; c < DC; ++c) y[r * DC + c] = r < n ? acc[c] : 0.0;
-  }
-}
-
-// y = Lp^T x
-template <int NT, int DC>
-__device__ __forceinline__ void mv_pack_t(const double* P, const double* x, double* y, int n, double* red) {
-  using S = Solve2Shape<NT>;
-  const int tid = threadIdx.x, col = tid % NT, part = tid / NT;
-  double acc[DC];
-#pragma unroll
-  for (int c = 0; c < DC; ++c) acc[c] = 0.0;
-  if (col < n) {
-#pragma unroll 4
-    for (int i = 0; i < S::SPAN; ++i) {
-      const int m = part * S::SPAN + i;
-      if (m < n && m >= col) {
-        const double v = P[packed_row_offset(m) + col];
-#pragma unroll
-        for (int c = 0; c < DC; ++c) acc[c] = fma(v, x[m * DC + c], acc[c]);
-      }
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < DC; ++c) red[(part * NT + col) * DC + c] = acc[c];
-  __syncthreads();
-  if (part == 0) {
-#pragma unroll
-    for (int c = 0; c < DC; ++c) {
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < S::PARTS; ++q) s += red[(q * NT + col) * DC + c];
-      y[col * DC + c] = col < n ? s : 0.0;
-    }
-  }
-}
 
 // ============================================================================================
 // Producer/consumer version (n == NT, n even): warp NCW (the last warp) streams the step blocks
