@@ -184,3 +184,27 @@ def test_host_input_npd_coordinates_match_device_path():
         pkg.recursive_factorize(pkg.BlockTridiagonalMatrix(torch.from_numpy(diag).cuda(), torch.from_numpy(A.sub).cuda()))
     a, b = e_host.value, e_dev.value
     assert (a.pivot, a.level, a.member, a.block) == (b.pivot, b.level, b.member, b.block)
+
+
+@pytest.mark.parametrize("N,n,rho,cross,bad", [
+    (3000, 64, 8, 64, [(1234, 5), (1500, 40)]),   # wide level: factor_level_kernel<64>
+    (600, 64, 8, 64, [(301, 63)]),                 # single-wave levels: factor_stream_kernel
+    (70, 64, 8, 64, [(20, 0), (61, 7)]),           # deep level + base
+    (5000, 6, 8, 64, [(777, 2), (778, 0)]),        # n <= 8: factor_small_kernel
+    (2000, 40, 3, 16, [(999, 17)]),                # n = 40 padded to 64
+    (6000, 64, 8, 64, [(9 * 20, 3)]),              # a level-0 separator: fails at level 1
+])
+def test_npd_coordinates_every_kernel_vs_oracle(N, n, rho, cross, bad):
+    """A non-positive pivot reports the oracle's (pivot, level, member, block) -- the reference's
+    earliest-step, lowest-member rule -- whichever factor kernel the level runs on."""
+    A, _ = pkg.generate_spd_btd(N, n, 1, seed=9)
+    diag = A.diag.copy()
+    for blk, i in bad:
+        diag[blk, i, i] = -1.0e3
+    with pytest.raises(port.OracleNPD) as eo:
+        port.factorize(diag, A.sub, cross, rho)
+    with pytest.raises(pkg.NotPositiveDefinite) as eg:
+        pkg.recursive_factorize(pkg.BlockTridiagonalMatrix(torch.from_numpy(diag).cuda(), torch.from_numpy(A.sub).cuda()),
+                                pkg.RecursionConfig(crossover=cross, segment_length=rho))
+    o, g = eo.value, eg.value
+    assert (g.pivot, g.level, g.member, g.block) == (o.pivot, o.level, o.member, o.block)
