@@ -164,13 +164,15 @@ template <int NT>
 cudaError_t launch_factor(const btd::FactorArgs& a, unsigned grid, cudaStream_t s) {
   using S = btd::FactorShape<NT>;
   static bool configured = false;
+  // BTD_ONE_CTA=1 (experiment): inflate the dynamic shared memory so only one CTA fits per SM
+  static const size_t smem = (getenv("BTD_ONE_CTA") != nullptr && NT == 64) ? (size_t)150 * 1024 : S::SMEM;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(btd::factor_level_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)S::SMEM);
+                                         (int)smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  btd::factor_level_kernel<NT><<<grid, S::NTHREADS, S::SMEM, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
+  btd::factor_level_kernel<NT><<<grid, S::NTHREADS, smem, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 

@@ -19,6 +19,19 @@
 
 namespace btd {
 
+#ifdef BTD_PHASE_PROF
+#define BTD_SPH(i)                                                          \
+  do {                                                                      \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                              \
+      long long _now = clock64();                                           \
+      atomicAdd(&g_phase_cycles[i], (unsigned long long)(_now - _sp_last)); \
+      _sp_last = _now;                                                      \
+    }                                                                       \
+  } while (0)
+#else
+#define BTD_SPH(i)
+#endif
+
 template <int NT>
 struct Solve2Shape {
   static constexpr int NTHREADS = 4 * NT;   // 4 threads per output row / column
@@ -74,10 +87,10 @@ __device__ __forceinline__ void step_kind(int mode, int J, int idx, int& kind, i
   }
 }
 
-// y (+)= sign * M x, M dense NT x NT (row-major, shared), x NT x DC
+// Row form: s[c] = sum_m M[r][m] x[m][c] for the thread's row r = tid / 4 (valid on the 4 lanes
+// of the row quad); rotated double2 reads keep the quad's rows conflict-free.
 template <int NT, int DC>
-__device__ __forceinline__ void fmv_full(const double* __restrict__ M, const double* __restrict__ x, double* y,
-                                         double sign, bool acc_into) {
+__device__ __forceinline__ void mv_rows(const double* __restrict__ M, const double* __restrict__ x, double (&s)[DC]) {
   constexpr int SPAN = NT / 4, NP = SPAN / 2, PM = NP - 1;
   const int tid = threadIdx.x, r = tid >> 2, part = tid & 3;
   const double* Mr = M + r * NT + part * SPAN;
@@ -89,35 +102,28 @@ __device__ __forceinline__ void fmv_full(const double* __restrict__ M, const dou
   for (int q = 0; q < NP; ++q) {
     const int qq = (q + r + 2 * part) & PM;
     const double2 v = *reinterpret_cast<const double2*>(Mr + 2 * qq);
-    if (DC == 1) {
-      const double2 xv = *reinterpret_cast<const double2*>(xp + 2 * qq);
-      a0[0] = fma(v.x, xv.x, a0[0]);
-      a1[0] = fma(v.y, xv.y, a1[0]);
-    } else {
 #pragma unroll
-      for (int c = 0; c < DC; ++c) {
-        a0[c] = fma(v.x, xp[(2 * qq) * DC + c], a0[c]);
-        a1[c] = fma(v.y, xp[(2 * qq + 1) * DC + c], a1[c]);
-      }
+    for (int c = 0; c < DC; ++c) {
+      a0[c] = fma(v.x, xp[(2 * qq) * DC + c], a0[c]);
+      a1[c] = fma(v.y, xp[(2 * qq + 1) * DC + c], a1[c]);
     }
   }
 #pragma unroll
   for (int c = 0; c < DC; ++c) {
-    double t = a0[c] + a1[c];
-    t += __shfl_xor_sync(0xffffffffu, t, 1);
-    t += __shfl_xor_sync(0xffffffffu, t, 2);
-    if (part == 0) y[r * DC + c] = acc_into ? fma(sign, t, y[r * DC + c]) : sign * t;
+    double v = a0[c] + a1[c];
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    s[c] = v;
   }
 }
 
-// y = Lp x (packed lower, zero padded rows)
+// Row form of the packed lower-triangular Linv: s[c] = sum_{m <= r} Lp[r][m] x[m][c].
 template <int NT, int DC>
-__device__ __forceinline__ void fmv_pack(const double* __restrict__ P, const double* __restrict__ x, double* y) {
+__device__ __forceinline__ void mv_pack_rows(const double* __restrict__ P, const double* __restrict__ x, double (&s)[DC]) {
   constexpr int SPAN = NT / 4, NP = SPAN / 2, PM = NP - 1;
   const int tid = threadIdx.x, r = tid >> 2, part = tid & 3;
   const double* row = P + packed_row_offset(r);
   const int npr = (r + 2) >> 1;  // pairs in row r
-  const double* xp = x;
   double a0[DC], a1[DC];
 #pragma unroll
   for (int c = 0; c < DC; ++c) a0[c] = a1[c] = 0.0;
@@ -126,92 +132,157 @@ __device__ __forceinline__ void fmv_pack(const double* __restrict__ P, const dou
     const int pq = part * NP + ((q + r + 2 * part) & PM);
     if (pq < npr) {
       const double2 v = *reinterpret_cast<const double2*>(row + 2 * pq);
-      if (DC == 1) {
-        const double2 xv = *reinterpret_cast<const double2*>(xp + 2 * pq);
-        a0[0] = fma(v.x, xv.x, a0[0]);
-        a1[0] = fma(v.y, xv.y, a1[0]);
-      } else {
 #pragma unroll
-        for (int c = 0; c < DC; ++c) {
-          a0[c] = fma(v.x, xp[(2 * pq) * DC + c], a0[c]);
-          a1[c] = fma(v.y, xp[(2 * pq + 1) * DC + c], a1[c]);
-        }
+      for (int c = 0; c < DC; ++c) {
+        a0[c] = fma(v.x, x[(2 * pq) * DC + c], a0[c]);
+        a1[c] = fma(v.y, x[(2 * pq + 1) * DC + c], a1[c]);
       }
     }
   }
 #pragma unroll
   for (int c = 0; c < DC; ++c) {
-    double t = a0[c] + a1[c];
-    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    double v = a0[c] + a1[c];
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    s[c] = v;
+  }
+}
+
+// Transposed form on warps [0, NT/16): v[h][c] = sum_m M[m][col + h] x[m][c] for the column pair
+// col = 16 warp + 2 (lane % 8).  A warp owns 16 columns: lane = pair + 8 part, part sweeping rows
+// part, part + 4, ...; each row's 16 columns are one contiguous 128-byte run (conflict-free
+// double2 reads), and the 4 parts are reduced with xor shuffles (result on every lane).
+// PACKED: M is the packed lower triangle (only m >= col contributes; pairs past the row are skipped).
+template <int NT, int DC, bool PACKED>
+__device__ __forceinline__ void mtv(const double* __restrict__ M, const double* __restrict__ x, double (&v)[2][DC]) {
+  constexpr int CW = NT < 16 ? NT : 16, PR = CW / 2, PT = 32 / PR;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int part = lane / PR, col = CW * w + 2 * (lane % PR);
+  double a[2][2][DC];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int c = 0; c < DC; ++c) a[0][h][c] = a[1][h][c] = 0.0;
+#pragma unroll
+  for (int i = 0; i < NT / PT; ++i) {
+    const int m = part + PT * i;
+    double2 e = make_double2(0.0, 0.0);
+    if (!PACKED) e = *reinterpret_cast<const double2*>(M + m * NT + col);
+    else if (col <= m) e = *reinterpret_cast<const double2*>(M + packed_row_offset(m) + col);
+#pragma unroll
+    for (int c = 0; c < DC; ++c) {
+      const double xv = x[m * DC + c];
+      a[i & 1][0][c] = fma(e.x, xv, a[i & 1][0][c]);
+      a[i & 1][1][c] = fma(e.y, xv, a[i & 1][1][c]);
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int c = 0; c < DC; ++c) {
+      double s = a[0][h][c] + a[1][h][c];
+#pragma unroll
+      for (int o = PR; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      v[h][c] = s;
+    }
+}
+
+// Row form at NT == 64 without the rotated reads: warp w owns rows 8w..8w+7 and lane l the column
+// pair (2l, 2l+1), so each row read is one contiguous conflict-free 512-byte run and x[2l..2l+1]
+// is loaded once into registers; the 8 row partials are reduced across the warp by a
+// transposing butterfly (4 + 2 + 1 + 2 shuffles).  The total of row 8w + lane/4 (= tid/4, the
+// mv_rows mapping) is returned on the 4 lanes of that row's quad.
+template <int DC, bool PACKED>
+__device__ __forceinline__ void mv64(const double* __restrict__ M, const double* __restrict__ x, double (&s)[DC]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c2 = 2 * lane;
+  double x0[DC], x1[DC], v[8][DC];
+  if (DC == 1) {
+    const double2 xv = *reinterpret_cast<const double2*>(x + c2);
+    x0[0] = xv.x;
+    x1[0] = xv.y;
+  } else {
+#pragma unroll
+    for (int c = 0; c < DC; ++c) {
+      x0[c] = x[c2 * DC + c];
+      x1[c] = x[(c2 + 1) * DC + c];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = 8 * w + i;
+    double2 e = make_double2(0.0, 0.0);
+    if (!PACKED) e = *reinterpret_cast<const double2*>(M + r * 64 + c2);
+    else if (c2 <= r) e = *reinterpret_cast<const double2*>(M + packed_row_offset(r) + c2);
+#pragma unroll
+    for (int c = 0; c < DC; ++c) v[i][c] = fma(e.x, x0[c], e.y * x1[c]);
+  }
+  const bool b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1;
+#pragma unroll
+  for (int c = 0; c < DC; ++c) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double snd = b4 ? v[i][c] : v[i + 4][c], kp = b4 ? v[i + 4][c] : v[i][c];
+      v[i][c] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const double snd = b3 ? v[i][c] : v[i + 2][c], kp = b3 ? v[i + 2][c] : v[i][c];
+      v[i][c] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+    }
+    {
+      const double snd = b2 ? v[0][c] : v[1][c], kp = b2 ? v[1][c] : v[0][c];
+      v[0][c] = kp + __shfl_xor_sync(0xffffffffu, snd, 4);
+    }
+    double t = v[0][c];
     t += __shfl_xor_sync(0xffffffffu, t, 2);
-    if (part == 0) y[r * DC + c] = t;
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    s[c] = t;
   }
 }
 
-// y (+)= sign * M^T x (dense) ; 4 row slices reduced through `red`
 template <int NT, int DC>
-__device__ __forceinline__ void fmv_full_t(const double* __restrict__ M, const double* __restrict__ x, double* y,
-                                           double sign, bool acc_into, double* red) {
-  constexpr int SPAN = NT / 4;
-  const int tid = threadIdx.x, col = tid % NT, part = tid / NT;
-  double a0[DC], a1[DC];
-#pragma unroll
-  for (int c = 0; c < DC; ++c) a0[c] = a1[c] = 0.0;
-#pragma unroll
-  for (int i = 0; i < SPAN; i += 2) {
-    const int m = part * SPAN + i;
-    const double v0 = M[m * NT + col], v1 = M[(m + 1) * NT + col];
-#pragma unroll
-    for (int c = 0; c < DC; ++c) {
-      a0[c] = fma(v0, x[m * DC + c], a0[c]);
-      a1[c] = fma(v1, x[(m + 1) * DC + c], a1[c]);
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < DC; ++c) red[(part * NT + col) * DC + c] = a0[c] + a1[c];
-  csync<NT>();
-  if (part == 0) {
-#pragma unroll
-    for (int c = 0; c < DC; ++c) {
-      const double s4 = (red[col * DC + c] + red[(NT + col) * DC + c]) +
-                        (red[(2 * NT + col) * DC + c] + red[(3 * NT + col) * DC + c]);
-      y[col * DC + c] = acc_into ? fma(sign, s4, y[col * DC + c]) : sign * s4;
-    }
-  }
+__device__ __forceinline__ void mv_full_rows(const double* M, const double* x, double (&s)[DC]) {
+#ifndef BTD_SOLVE_ROTATED
+  if constexpr (NT == 64) { mv64<DC, false>(M, x, s); return; }
+#endif
+  mv_rows<NT, DC>(M, x, s);
+}
+template <int NT, int DC>
+__device__ __forceinline__ void mv_packed_rows(const double* M, const double* x, double (&s)[DC]) {
+#ifndef BTD_SOLVE_ROTATED
+  if constexpr (NT == 64) { mv64<DC, true>(M, x, s); return; }
+#endif
+  mv_pack_rows<NT, DC>(M, x, s);
 }
 
-// y = Lp^T x
-template <int NT, int DC>
-__device__ __forceinline__ void fmv_pack_t(const double* __restrict__ P, const double* __restrict__ x, double* y,
-                                           double* red) {
-  constexpr int SPAN = NT / 4;
-  const int tid = threadIdx.x, col = tid % NT, part = tid / NT;
-  double a0[DC], a1[DC];
-#pragma unroll
-  for (int c = 0; c < DC; ++c) a0[c] = a1[c] = 0.0;
-#pragma unroll
-  for (int i = 0; i < SPAN; i += 2) {
-    const int m = part * SPAN + i;
-    if (m + 1 >= col) {  // rows m, m+1 (row m contributes only if m >= col; its pad is zero)
-      const double v0 = (m >= col) ? P[packed_row_offset(m) + col] : 0.0;
-      const double v1 = P[packed_row_offset(m + 1) + col];
-#pragma unroll
-      for (int c = 0; c < DC; ++c) {
-        a0[c] = fma(v0, x[m * DC + c], a0[c]);
-        a1[c] = fma(v1, x[(m + 1) * DC + c], a1[c]);
-      }
+// Segment bounds of the persistent loops, with the next segment's separators loaded one segment
+// ahead (their global-load latency would otherwise stall every segment start).
+struct SegBounds {
+  long long start, stop;
+  int nlo, nhi;
+  __device__ SegBounds(const SolveArgs& a, int mode, int k, int K) {
+    start = stop = 0;
+    nlo = nhi = 0;
+    if (mode == kSolveBase) {
+      start = 0;
+      stop = a.N;
+    } else if (k < K) {
+      start = (long long)a.seps[k] + 1;
+      stop = a.seps[k + 1];
     }
   }
-#pragma unroll
-  for (int c = 0; c < DC; ++c) red[(part * NT + col) * DC + c] = a0[c] + a1[c];
-  csync<NT>();
-  if (part == 0) {
-#pragma unroll
-    for (int c = 0; c < DC; ++c)
-      y[col * DC + c] = (red[col * DC + c] + red[(NT + col) * DC + c]) +
-                        (red[(2 * NT + col) * DC + c] + red[(3 * NT + col) * DC + c]);
+  __device__ __forceinline__ void advance(const SolveArgs& a, int mode, int kn, int K) {
+    if (mode != kSolveBase && kn < K) {
+      nlo = __ldg(a.seps + kn);
+      nhi = __ldg(a.seps + kn + 1);
+    }
   }
-}
+  __device__ __forceinline__ void next() {
+    start = (long long)nlo + 1;
+    stop = nhi;
+  }
+};
 
 template <int NT, int DC>
 struct TmaShape {
@@ -223,7 +294,7 @@ struct TmaShape {
 #endif
   static constexpr int STAGES = NT == 64 ? (DC > 1 ? 3 : BTD_TMA_STAGES64) : 8;
   static constexpr int STAGE = S::FULL + S::PACK + NT * DC;  // doubles per slot
-  static constexpr size_t SMEM = sizeof(double) * ((size_t)STAGES * STAGE + (size_t)(4 + S::ZMAX + S::PARTS) * NT * DC) +
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)STAGES * STAGE + (size_t)(4 + S::ZMAX) * NT * DC) +
                                  2 * STAGES * sizeof(unsigned long long);
 };
 
@@ -238,8 +309,7 @@ __global__ void __launch_bounds__(TmaShape<NT, DC>::NTHREADS) solve_tma_kernel(S
   double* u = t + NT * DC;
   double* corr = u + NT * DC;
   double* zc = corr + 2 * NT * DC;
-  double* red = zc + S::ZMAX * NT * DC;
-  unsigned long long* full_bar = reinterpret_cast<unsigned long long*>(red + S::PARTS * NT * DC);
+  unsigned long long* full_bar = reinterpret_cast<unsigned long long*>(zc + S::ZMAX * NT * DC);
   unsigned long long* empty_bar = full_bar + STAGES;
   if (error_raised(a.err)) return;
   const int n = NT, d = a.d, mode = a.mode;
@@ -266,9 +336,10 @@ __global__ void __launch_bounds__(TmaShape<NT, DC>::NTHREADS) solve_tma_kernel(S
       unsigned phase = 0;
       constexpr unsigned fb = NT * NT * sizeof(double), pb = S::PACK * sizeof(double);
       const unsigned vb = (unsigned)(n * d * sizeof(double));
+      SegBounds sb(a, mode, blockIdx.x, K);
       for (int k = blockIdx.x; k < K; k += gridDim.x) {
-        const long long start = mode == kSolveBase ? 0 : (long long)a.seps[k] + 1;
-        const long long stop = mode == kSolveBase ? a.N : (long long)a.seps[k + 1];
+        const long long start = sb.start, stop = sb.stop;
+        sb.advance(a, mode, k + gridDim.x, K);  // the next segment's separators load behind this one
         const int J = (int)(stop - start);
         const int ns = nsteps(mode, J);
         for (int idx = 0; idx < ns; ++idx) {
@@ -293,6 +364,9 @@ __global__ void __launch_bounds__(TmaShape<NT, DC>::NTHREADS) solve_tma_kernel(S
           if (!vec_bulk) vec = nullptr;
           mbar_wait(&empty_bar[slot], phase ^ 1);
           double* st = ring + slot * STAGE;
+#ifdef BTD_SOLVE_NOLOAD  // diagnostic: consumers run on stale slot contents (pure consumer time)
+          full = pack = vec = nullptr;
+#endif
           mbar_arrive_expect_tx(&full_bar[slot], (full ? fb : 0) + (pack ? pb : 0) + (vec ? vb : 0));
           if (full) tma_load_1d(st, full, fb, &full_bar[slot]);
           if (pack) tma_load_1d(st + S::FULL, pack, pb, &full_bar[slot]);
@@ -302,101 +376,196 @@ __global__ void __launch_bounds__(TmaShape<NT, DC>::NTHREADS) solve_tma_kernel(S
             phase ^= 1;
           }
         }
+        sb.next();
       }
     }
     return;
   }
 
   // ===================== consumer warps =====================
+  // Two dependent mat-vecs per step and one barrier after each (the slot is released per warp):
+  // row-form products (forward sweep, C_R fold) on all consumer warps, 4 threads per row;
+  // transposed products (backward sweep, C_L fold) on the first TW warps with every part of a
+  // column inside one warp (xor-shuffle reduction, no shared-memory partials).
+  constexpr int TW = NT < 16 ? 1 : NT / 16;
+  constexpr int CW = NT < 16 ? NT : 16, PR = CW / 2;
+  const int rr = tid >> 2;
+  const bool rlead = (tid & 3) == 0;
+  const int tc = CW * warp + 2 * (lane % PR);
+  const bool tlead = warp < TW && lane < PR;
   int slot = 0;
   unsigned phase = 0;
+#ifdef BTD_PHASE_PROF
+  long long _sp_last = clock64();
+#endif
+  SegBounds sb(a, mode, blockIdx.x, K);
   for (int k = blockIdx.x; k < K; k += gridDim.x) {
-    const long long start = mode == kSolveBase ? 0 : (long long)a.seps[k] + 1;
-    const long long stop = mode == kSolveBase ? a.N : (long long)a.seps[k + 1];
+    const long long start = sb.start, stop = sb.stop;
+    sb.advance(a, mode, k + gridDim.x, K);  // the next segment's separators load behind this one
     const int J = (int)(stop - start);
     const int ns = nsteps(mode, J);
     for (int idx = 0; idx < ns; ++idx) {
       int kind, j;
       step_kind(mode, J, idx, kind, j);
       const long long row = start + j;
+      BTD_SPH(0);
       mbar_wait(&full_bar[slot], phase);
+      BTD_SPH(1);
+#ifdef BTD_SOLVE_NOMATH  // diagnostic: consumers only release the slots (pure producer/memory time)
+      kind = kStepNone;
+#endif
       const double* sf = ring + slot * STAGE;
       const double* sp = sf + S::FULL;
       const double* sv = sp + S::PACK;
-      if (kind == kStepF) {
-        for (int e = tid; e < NT * DC; e += NTH) {
-          const int r = e / DC, c = e % DC;
-          double v = 0.0;
-          if (c < dc) v = vec_bulk ? sv[r * d + c] : a.rhs[row * ps + (size_t)r * d + c0 + c];
-          if (mode == kSolveUp) {
-            if (j == 0) v -= corr[e];
-            if (j == J - 1) v -= corr[NT * DC + e];
-          }
-          t[e] = v;
+      // b_j[r][c] with the up-pass boundary corrections
+      auto bval = [&](int r, int c) -> double {
+        double v = 0.0;
+        if (c < dc) v = vec_bulk ? sv[r * d + c] : a.rhs[row * ps + (size_t)r * d + c0 + c];
+        if (mode == kSolveUp) {
+          if (j == 0) v -= corr[r * DC + c];
+          if (j == J - 1) v -= corr[NT * DC + r * DC + c];
         }
-        csync<NT>();
+        return v;
+      };
+      if (kind == kStepNone) {
+      } else if (kind == kStepF) {
+        // t = b_j - L_{j,j-1} z_{j-1}
         if (j > 0) {
-          fmv_full<NT, DC>(sf, u, t, -1.0, true);
-          csync<NT>();
+          double sm[DC];
+          mv_full_rows<NT, DC>(sf, u, sm);
+          if (rlead) {
+#pragma unroll
+            for (int c = 0; c < DC; ++c) t[rr * DC + c] = bval(rr, c) - sm[c];
+          }
+        } else {
+          for (int e = tid; e < NT * DC; e += NTH) t[e] = bval(e / DC, e % DC);
         }
-        fmv_pack<NT, DC>(sp, t, u);  // z_j -> u
+        BTD_SPH(2);
         csync<NT>();
-        double* zdst = j < S::ZMAX ? zc + j * NT * DC : nullptr;
-        for (int e = tid; e < NT * DC; e += NTH) {
-          if (zdst) zdst[e] = u[e];
-          else if ((e % DC) < dc) a.x[row * ps + (size_t)(e / DC) * d + c0 + e % DC] = u[e];
+        BTD_SPH(3);
+        // z_j = Linv_j t
+        double sm[DC];
+        mv_packed_rows<NT, DC>(sp, t, sm);
+        if (rlead) {
+          double* zdst = j < S::ZMAX ? zc + j * NT * DC : nullptr;
+#pragma unroll
+          for (int c = 0; c < DC; ++c) {
+            u[rr * DC + c] = sm[c];
+            if (zdst) zdst[rr * DC + c] = sm[c];
+            else if (c < dc) a.x[row * ps + (size_t)rr * d + c0 + c] = sm[c];
+          }
         }
+        BTD_SPH(4);
+        csync<NT>();
+        BTD_SPH(5);
       } else if (kind == kStepB) {
         const double* zsrc = j < S::ZMAX ? zc + j * NT * DC : nullptr;
-        for (int e = tid; e < NT * DC; e += NTH) {
-          const int r = e / DC, c = e % DC;
-          t[e] = zsrc ? zsrc[e] : (c < dc ? a.x[row * ps + (size_t)r * d + c0 + c] : 0.0);
-        }
-        csync<NT>();
-        if (j < J - 1) {
-          fmv_full_t<NT, DC>(sf, u, t, -1.0, true, red);
+        auto zval = [&](int r, int c) -> double {
+          return zsrc ? zsrc[r * DC + c] : (c < dc ? a.x[row * ps + (size_t)r * d + c0 + c] : 0.0);
+        };
+        const double* src = zsrc;
+        if (j < J - 1) {  // t = z_j - L_{j+1,j}^T w_{j+1}
+          if (warp < TW) {
+            double v[2][DC];
+            mtv<NT, DC, false>(sf, u, v);
+            if (tlead) {
+#pragma unroll
+              for (int c = 0; c < DC; ++c) {
+                t[tc * DC + c] = zval(tc, c) - v[0][c];
+                t[(tc + 1) * DC + c] = zval(tc + 1, c) - v[1][c];
+              }
+            }
+          }
+          BTD_SPH(6);
           csync<NT>();
+          BTD_SPH(7);
+          src = t;
+        } else if (!zsrc) {
+          for (int e = tid; e < NT * DC; e += NTH) t[e] = zval(e / DC, e % DC);
+          csync<NT>();
+          src = t;
         }
-        fmv_pack_t<NT, DC>(sp, t, u, red);  // w_j -> u
-        csync<NT>();
-        if (mode != kSolveDown) {
-          for (int e = tid; e < NT * DC; e += NTH)
-            if ((e % DC) < dc) a.x[row * ps + (size_t)(e / DC) * d + c0 + e % DC] = u[e];
+        // w_j = Linv_j^T t
+        if (warp < TW) {
+          double v[2][DC];
+          mtv<NT, DC, true>(sp, src, v);
+          if (tlead) {
+#pragma unroll
+            for (int c = 0; c < DC; ++c)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                u[(tc + h) * DC + c] = v[h][c];
+                if (mode != kSolveDown && c < dc) a.x[row * ps + (size_t)(tc + h) * d + c0 + c] = v[h][c];
+              }
+          }
         }
-      } else if (mode == kSolveDown) {  // fold: f_R = C_R w_last ; f_L = C_L^T w_0
-        if (kind == kStepCR)
-          fmv_full<NT, DC>(sf, u, t, 1.0, false);
-        else
-          fmv_full_t<NT, DC>(sf, u, t, 1.0, false, red);
+        BTD_SPH(8);
         csync<NT>();
+        BTD_SPH(9);
+      } else if (mode == kSolveDown) {  // fold: f_R = C_R w_last ; f_L = C_L^T w_0 (no barrier needed)
         double* dst = (kind == kStepCR ? a.fr : a.fl) + (size_t)k * ps;
-        for (int e = tid; e < NT * DC; e += NTH)
-          if ((e % DC) < dc) dst[(size_t)(e / DC) * d + c0 + e % DC] = t[e];
+        if (kind == kStepCR) {
+          double sm[DC];
+          mv_full_rows<NT, DC>(sf, u, sm);
+          if (rlead) {
+#pragma unroll
+            for (int c = 0; c < DC; ++c)
+              if (c < dc) dst[(size_t)rr * d + c0 + c] = sm[c];
+          }
+        } else if (warp < TW) {
+          double v[2][DC];
+          mtv<NT, DC, false>(sf, u, v);
+          if (tlead) {
+#pragma unroll
+            for (int c = 0; c < DC; ++c)
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+                if (c < dc) dst[(size_t)(tc + h) * d + c0 + c] = v[h][c];
+          }
+        }
       } else {  // up: boundary corrections C_L x_L -> corr[0], C_R^T x_R -> corr[1]
         const double* xs = a.xsep + (size_t)(kind == kStepCL ? k : k + 1) * ps;
         for (int e = tid; e < NT * DC; e += NTH) {
           const int r = e / DC, c = e % DC;
-          t[e] = c < dc ? (vec_bulk ? sv[r * d + c] : xs[(size_t)r * d + c0 + c]) : 0.0;
+          const double v = c < dc ? (vec_bulk ? sv[r * d + c] : xs[(size_t)r * d + c0 + c]) : 0.0;
+          t[e] = v;
+          if (c < dc) {
+            const size_t off = (size_t)r * d + c0 + c;
+            if (kind == kStepCL) a.x[(size_t)(start - 1) * ps + off] = v;
+            if (kind == kStepCR && k == K - 1) a.x[(size_t)stop * ps + off] = v;
+          }
         }
         csync<NT>();
-        if (kind == kStepCL)
-          fmv_full<NT, DC>(sf, t, corr, 1.0, false);
-        else
-          fmv_full_t<NT, DC>(sf, t, corr + NT * DC, 1.0, false, red);
-        for (int e = tid; e < NT * DC; e += NTH) {
-          if ((e % DC) >= dc) continue;
-          const size_t off = (size_t)(e / DC) * d + c0 + e % DC;
-          if (kind == kStepCL) a.x[(size_t)(start - 1) * ps + off] = t[e];
-          if (kind == kStepCR && k == K - 1) a.x[(size_t)stop * ps + off] = t[e];
+        if (kind == kStepCL) {
+          double sm[DC];
+          mv_full_rows<NT, DC>(sf, t, sm);
+          if (rlead) {
+#pragma unroll
+            for (int c = 0; c < DC; ++c) corr[rr * DC + c] = sm[c];
+          }
+        } else if (warp < TW) {
+          double v[2][DC];
+          mtv<NT, DC, false>(sf, t, v);
+          if (tlead) {
+#pragma unroll
+            for (int c = 0; c < DC; ++c) {
+              corr[NT * DC + tc * DC + c] = v[0][c];
+              corr[NT * DC + (tc + 1) * DC + c] = v[1][c];
+            }
+          }
         }
+        csync<NT>();
       }
-      csync<NT>();  // slot and work panels fully consumed
-      if (lane == 0) mbar_arrive(&empty_bar[slot]);
+      BTD_SPH(10);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[slot]);  // this warp is done with the slot
+      BTD_SPH(11);
       if (++slot == STAGES) {
         slot = 0;
         phase ^= 1;
       }
     }
+    sb.next();
   }
 }
 
