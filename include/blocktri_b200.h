@@ -174,8 +174,17 @@ int btd_kalman_normal_equations(int64_t horizon, int64_t state_dim, int64_t obs_
                                 double* diag, double* sub, double* rhs, void* workspace, void* stream,
                                 btd_status* st);
 
-/* Process-wide count of kernels this library has launched (evidence for bench.py gpu_launches). */
+/* Process-wide count of kernels this library has launched (evidence for bench.py gpu_launches);
+ * a replayed CUDA graph adds the kernel launches it contains. */
 long long btd_launch_count(void);
+
+/* CUDA graphs (no reference counterpart: replaces the per-kernel launches of the paper's batched
+ * BLAS calls, §5).  With device-resident inputs, btd_factorize / btd_solve (and the
+ * partial variants) capture their whole launch sequence -- every level, assembly and the base --
+ * into one graph per (shape, config, buffer addresses) and replay it on later calls with the same
+ * buffers.  Enabled by default (environment BTD_GRAPHS=0 disables); returns the previous setting.
+ * Disabling drops the cached graphs. */
+int btd_set_graphs(int32_t enable);
 
 #ifdef __cplusplus
 }

@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -565,6 +567,112 @@ cudaError_t export_reduced(const btd_hierarchy* h, const double* cd, const doubl
 
 }  // namespace
 
+namespace {
+
+// ---------------------------------------------------------------------------------------------
+// CUDA graphs: the whole launch sequence of a factorization (every level, the assemblies and the
+// base) or of a solve is captured once per (shape, config, buffer addresses) and replayed with
+// one cudaGraphLaunch.  torch's caching allocator hands the same addresses back to repeated
+// factorizations of the same shape, so steady-state calls hit the cache.  BTD_GRAPHS=0 disables.
+// ---------------------------------------------------------------------------------------------
+struct GraphKey {  // all 8-byte fields: no padding, so memcmp ordering is well defined
+  int64_t kind;  // 0 factor, 1 + phase: solve
+  int64_t N, n, crossover, rho, max_levels, auto_cross, nlevels, extra;
+  const void* ptr[7];
+  int64_t device = 0;
+  bool operator<(const GraphKey& o) const {
+    return std::memcmp(this, &o, sizeof(GraphKey)) < 0;
+  }
+};
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  long long launches = 0;
+  unsigned long long last_use = 0;
+};
+std::mutex g_graph_mu;
+std::map<GraphKey, GraphEntry> g_graphs;
+unsigned long long g_graph_clock = 0;
+constexpr size_t kMaxGraphs = 32;
+
+std::atomic<int> g_graphs_on{-1};  // -1: not read from BTD_GRAPHS yet
+
+bool graphs_enabled() {
+  int v = g_graphs_on.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* ev = getenv("BTD_GRAPHS");
+    v = (ev && ev[0] == '0') ? 0 : 1;
+    g_graphs_on.store(v, std::memory_order_relaxed);
+  }
+  return v == 1;
+}
+
+template <class F>
+int run_graphed(GraphKey key, cudaStream_t stream, btd_status* st, F&& enqueue) {
+  if (!graphs_enabled()) return enqueue();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  key.device = dev;
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    auto it = g_graphs.find(key);
+    if (it != g_graphs.end()) {
+      it->second.last_use = ++g_graph_clock;
+      cudaError_t e = cudaGraphLaunch(it->second.exec, stream);
+      if (e != cudaSuccess) return cuda_fail(st, e, "cudaGraphLaunch");
+      g_launches.fetch_add(it->second.launches, std::memory_order_relaxed);
+      return BTD_OK;
+    }
+  }
+  cudaStreamCaptureStatus cs;
+  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+    return enqueue();  // the caller is capturing already: just record into its graph
+  const long long before = g_launches.load();
+  if (cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return enqueue();
+  }
+  const int rc = enqueue();
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(stream, &graph);
+  const long long launches = g_launches.load() - before;
+  g_launches.fetch_sub(launches, std::memory_order_relaxed);  // counted when the graph runs
+  if (rc != BTD_OK || e != cudaSuccess || !graph) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    clear_status(st);
+    return enqueue();  // nothing ran during the failed capture: run the sequence directly
+  }
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return enqueue();
+  }
+  e = cudaGraphLaunch(exec, stream);
+  if (e != cudaSuccess) {
+    cudaGraphExecDestroy(exec);
+    return cuda_fail(st, e, "cudaGraphLaunch");
+  }
+  g_launches.fetch_add(launches, std::memory_order_relaxed);
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  if (g_graphs.size() >= kMaxGraphs) {  // evict the least recently used graph
+    auto lru = g_graphs.begin();
+    for (auto it = g_graphs.begin(); it != g_graphs.end(); ++it)
+      if (it->second.last_use < lru->second.last_use) lru = it;
+    cudaGraphExecDestroy(lru->second.exec);
+    g_graphs.erase(lru);
+  }
+  GraphEntry& ent = g_graphs[key];
+  if (ent.exec) cudaGraphExecDestroy(ent.exec);  // another thread captured the same key meanwhile
+  ent.exec = exec;
+  ent.launches = launches;
+  ent.last_use = ++g_graph_clock;
+  return BTD_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* btd_version(void) { return "blocktri_b200 0.1.0 (sm_100a)"; }
@@ -822,19 +930,11 @@ cudaError_t chunked_level0(btd_hierarchy* h, btd::FactorArgs a, const LevelPlan&
 // segments on a private copy stream, and each chunk's segments are factored as soon as their
 // blocks have landed, so the H2D transfer overlaps the level-0 elimination.
 
-static int factorize_impl(btd_hierarchy* h, const double* diag, const double* sub, void* persistent, void* scratch,
-                          void* stream_, int32_t check, btd_status* st, double* red_diag, double* red_sub,
-                          const HostSrc* host = nullptr) {
-  clear_status(st);
-  if (!h || !diag || !persistent || !scratch || (h->N > 1 && !sub)) {
-    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_factorize: NULL argument");
-    return BTD_ERR_INVALID_ARGUMENT;
-  }
-  cudaStream_t stream = (cudaStream_t)stream_;
-  char* pers = (char*)persistent;
-  char* scr = (char*)scratch;
-  h->persistent = pers;
-  h->factored = false;
+// Every device operation of one factorization, enqueued on `stream` (captured into a CUDA graph by
+// factorize_impl when the inputs are device resident).  Host state is not touched here.
+static int enqueue_factor(btd_hierarchy* h, const double* diag, const double* sub, char* pers, char* scr,
+                          cudaStream_t stream, btd_status* st, double* red_diag, double* red_sub,
+                          const HostSrc* host) {
   const int n = (int)h->n;
   btd::DevErr* err = (btd::DevErr*)(pers + h->off_err);
   btd::init_err_kernel<<<1, 1, 0, stream>>>(err); g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -850,7 +950,6 @@ static int factorize_impl(btd_hierarchy* h, const double* diag, const double* su
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(seps)");
-  h->nev = 0;
 
   if (host && (h->big || h->levels.empty())) {  // no chunking: one bulk copy, then the usual path
     const size_t nn = (size_t)h->n * h->n * sizeof(double);
@@ -893,8 +992,6 @@ static int factorize_impl(btd_hierarchy* h, const double* diag, const double* su
       prof_mark(h, stream);
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(big base)");
     }
-    h->pending_check = true;
-    if (check) return finish_check(h, stream, st);
     return BTD_OK;
   }
   for (size_t l = 0; l < h->levels.size(); ++l) {
@@ -952,6 +1049,35 @@ static int factorize_impl(btd_hierarchy* h, const double* diag, const double* su
     prof_mark(h, stream);
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(base kernel)");
   }
+  return BTD_OK;
+}
+
+static int factorize_impl(btd_hierarchy* h, const double* diag, const double* sub, void* persistent, void* scratch,
+                          void* stream_, int32_t check, btd_status* st, double* red_diag, double* red_sub,
+                          const HostSrc* host = nullptr) {
+  clear_status(st);
+  if (!h || !diag || !persistent || !scratch || (h->N > 1 && !sub)) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_factorize: NULL argument");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  cudaStream_t stream = (cudaStream_t)stream_;
+  char* pers = (char*)persistent;
+  char* scr = (char*)scratch;
+  h->persistent = pers;
+  h->factored = false;
+  h->nev = 0;
+  int rc;
+  if (host || h->profile) {  // the host path uses a second stream; profiling records events
+    rc = enqueue_factor(h, diag, sub, pers, scr, stream, st, red_diag, red_sub, host);
+  } else {
+    const GraphKey key{0, h->N, h->n, h->cfg.crossover, h->cfg.segment_length, h->cfg.max_levels,
+                       h->cfg.auto_crossover, (int64_t)h->levels.size(), h->partial ? 1 : 0,
+                       {diag, sub, pers, scr, red_diag, red_sub, nullptr}};
+    rc = run_graphed(key, stream, st, [&]() {
+      return enqueue_factor(h, diag, sub, pers, scr, stream, st, red_diag, red_sub, nullptr);
+    });
+  }
+  if (rc != BTD_OK) return rc;
   h->pending_check = true;
   if (check) return finish_check(h, stream, st);
   return BTD_OK;
@@ -1019,22 +1145,9 @@ int btd_solve_workspace(const btd_hierarchy* h, int64_t d, size_t* scratch_bytes
   return BTD_OK;
 }
 
-static int solve_impl(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, void* scratch, void* stream_,
-                      btd_status* st, int phase, const double* red_in, double* red_out) {
-  clear_status(st);
-  if (!h || !rhs || !x || !scratch || d < 1) {
-    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_solve: NULL argument or d < 1");
-    return BTD_ERR_INVALID_ARGUMENT;
-  }
-  if (!h->factored && !h->pending_check) {
-    set_status(st, BTD_ERR_NOT_FACTORED, "hierarchy must be factorized before solving");
-    return BTD_ERR_NOT_FACTORED;
-  }
-  if (d > INT_MAX / 2) {
-    set_status(st, BTD_ERR_UNSUPPORTED, "too many rhs columns");
-    return BTD_ERR_UNSUPPORTED;
-  }
-  cudaStream_t stream = (cudaStream_t)stream_;
+// Every device operation of one solve, enqueued on `stream` (captured into a CUDA graph by solve_impl).
+static int enqueue_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, void* scratch,
+                         cudaStream_t stream, btd_status* st, int phase, const double* red_in, double* red_out) {
   const char* pers = h->persistent;
   char* scr = (char*)scratch;
   const btd::DevErr* err = (const btd::DevErr*)(pers + h->off_err);
@@ -1186,6 +1299,30 @@ static int solve_impl(const btd_hierarchy* h, const double* rhs, double* x, int6
   return BTD_OK;
 }
 
+static int solve_impl(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, void* scratch, void* stream_,
+                      btd_status* st, int phase, const double* red_in, double* red_out) {
+  clear_status(st);
+  if (!h || !rhs || !x || !scratch || d < 1) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_solve: NULL argument or d < 1");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  if (!h->factored && !h->pending_check) {
+    set_status(st, BTD_ERR_NOT_FACTORED, "hierarchy must be factorized before solving");
+    return BTD_ERR_NOT_FACTORED;
+  }
+  if (d > INT_MAX / 2) {
+    set_status(st, BTD_ERR_UNSUPPORTED, "too many rhs columns");
+    return BTD_ERR_UNSUPPORTED;
+  }
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const GraphKey key{1 + phase, h->N, h->n, h->cfg.crossover, h->cfg.segment_length, h->cfg.max_levels,
+                     h->cfg.auto_crossover, (int64_t)h->levels.size(), d,
+                     {h->persistent, rhs, x, scratch, red_in, red_out, (const void*)(intptr_t)h->partial}};
+  return run_graphed(key, stream, st, [&]() {
+    return enqueue_solve(h, rhs, x, d, scratch, stream, st, phase, red_in, red_out);
+  });
+}
+
 int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t d, void* scratch, void* stream,
               btd_status* st) {
   if (h && h->partial) {
@@ -1270,6 +1407,17 @@ int btd_kernel_times(const btd_hierarchy* h, float* ms_out, int64_t cap, int64_t
     cudaEventElapsedTime(&ms_out[i], h->ev[2 * i], h->ev[2 * i + 1]);
   }
   return BTD_OK;
+}
+
+int btd_set_graphs(int32_t enable) {
+  const int prev = graphs_enabled() ? 1 : 0;
+  g_graphs_on.store(enable ? 1 : 0, std::memory_order_relaxed);
+  if (!enable) {  // drop the cached executables
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    for (auto& kv : g_graphs) cudaGraphExecDestroy(kv.second.exec);
+    g_graphs.clear();
+  }
+  return prev;
 }
 
 long long btd_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
