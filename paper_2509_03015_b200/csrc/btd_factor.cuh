@@ -227,6 +227,23 @@ __device__ __forceinline__ int panel_chain(double* DL, int p0, int lane) {
   return fail;
 }
 
+// C fragment read-modify-write (tile (tr, tc) -= acc) as one 16-byte access per lane: half the
+// shared-memory wavefronts of two 8-byte accesses on the LD = NT + 4 layout.
+template <int LD>
+__device__ __forceinline__ void sub_frag(double* DL, int tr, int tc, int lane, const double (&acc)[2]) {
+#ifdef BTD_SCALAR_FRAG
+  double* dst = DL + (tr * 8 + (lane >> 2)) * LD + tc * 8 + 2 * (lane & 3);
+  dst[0] -= acc[0];
+  dst[1] -= acc[1];
+#else
+  double2* dst = reinterpret_cast<double2*>(DL + (tr * 8 + (lane >> 2)) * LD + tc * 8 + 2 * (lane & 3));
+  double2 v = *dst;
+  v.x -= acc[0];
+  v.y -= acc[1];
+  *dst = v;
+#endif
+}
+
 // rank-8 update of one 8x8 tile (tr, tc) by panel p: A[tr][tc] -= L[tr][p] L[tc][p]^T
 template <int NT>
 __device__ __forceinline__ void tile_update(double* DL, int tr, int tc, int p0, int lane) {
@@ -236,9 +253,7 @@ __device__ __forceinline__ void tile_update(double* DL, int tr, int tc, int p0, 
   double acc[2] = {0.0, 0.0};
   dmma(acc, pa[0], pb[0]);
   dmma(acc, pa[4], pb[4]);
-  double* dst = DL + (tr * 8 + (lane >> 2)) * LD + tc * 8 + 2 * (lane & 3);
-  dst[0] -= acc[0];
-  dst[1] -= acc[1];
+  sub_frag<LD>(DL, tr, tc, lane, acc);
 }
 
 // Rank-8 updates by the panel at column p0 of the lower-triangular tile set
@@ -271,9 +286,7 @@ __device__ __forceinline__ void tile_update_tri(double* DL, int off, int m, int 
       double acc[2] = {0.0, 0.0};
       dmma(acc, a0[q], b0[q]);
       dmma(acc, a1[q], b1[q]);
-      double* dst = DL + (tr[q] * 8 + (lane >> 2)) * LD + tc[q] * 8 + 2 * (lane & 3);
-      dst[0] -= acc[0];
-      dst[1] -= acc[1];
+      sub_frag<LD>(DL, tr[q], tc[q], lane, acc);
     }
   }
 }
@@ -401,12 +414,10 @@ __device__ int potrf_trtri(double* DL, int* s_fail, unsigned long long* leaf_bar
         const int i0 = i0v[q];
         if (phase == 0) {  // strictly-upper scratch block (rows i0.., cols i0+b..)
           double* dst = DL + (i0 + trv[q] * 8 + (lane >> 2)) * LD + i0 + b + tcv[q] * 8 + 2 * (lane & 3);
-          dst[0] = acc[q][0];
-          dst[1] = acc[q][1];
+          *reinterpret_cast<double2*>(dst) = make_double2(acc[q][0], acc[q][1]);
         } else {
           double* dst = DL + (i0 + b + trv[q] * 8 + (lane >> 2)) * LD + i0 + tcv[q] * 8 + 2 * (lane & 3);
-          dst[0] = -acc[q][0];
-          dst[1] = -acc[q][1];
+          *reinterpret_cast<double2*>(dst) = make_double2(-acc[q][0], -acc[q][1]);
         }
       }
       named_sync(kBarA, NWA * 32);
@@ -685,9 +696,11 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
           const int r = rr * TS + i * 8 + (lane >> 2);
           const int c = cc * TS + jj * 8 + 2 * (lane & 3);
           if (!last) {
-            double* dst = DL + r * LD + c;
-            dst[0] = (r == c && r >= n) ? 1.0 : dst[0] - acc[s][i][jj][0];
-            dst[1] = (r == c + 1 && r >= n) ? 1.0 : dst[1] - acc[s][i][jj][1];
+            double2* dst = reinterpret_cast<double2*>(DL + r * LD + c);
+            double2 v = *dst;
+            v.x = (r == c && r >= n) ? 1.0 : v.x - acc[s][i][jj][0];
+            v.y = (r == c + 1 && r >= n) ? 1.0 : v.y - acc[s][i][jj][1];
+            *dst = v;
           } else if (r < n) {
             double* dst = args.Sr + (size_t)k * bs + (size_t)r * n;
             if (c < n) dst[c] = acc[s][i][jj][0];

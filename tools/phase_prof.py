@@ -6,7 +6,7 @@ Phases (btd_factor.cuh BTD_PHASE ids) are summed over CTA 0 of every factor laun
 import ctypes, os, sys
 sys.path.insert(0, '.')
 from paper_2509_03015_b200 import _native
-_native.LIB_PATH = os.path.abspath(os.path.join('tools', 'libblocktri_b200_prof.so'))
+_native.LIB_PATH = os.path.abspath(os.environ.get('BTD_PROF_LIB', os.path.join('tools', 'libblocktri_b200_prof.so')))
 import torch
 import paper_2509_03015_b200 as pkg
 L = _native.lib()
