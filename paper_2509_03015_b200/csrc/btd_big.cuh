@@ -244,19 +244,34 @@ struct BigPotrfArgs {
   const int* seps;
   long long N;
   int base_mode, j, n, level;
+  int csize;     // CTAs per segment (a thread-block cluster when > 1)
   DevErr* err;
 };
 
-// Blocked Cholesky + inverse of an n x n block (n = 64 NB), one CTA per segment.
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// Blocked Cholesky + inverse of an n x n block (n = 64 NB).  One segment per thread-block
+// cluster of `csize` CTAs (csize = 1: one CTA per segment): rank 0 factors the 64 x 64 diagonal
+// tiles (potrf_trtri), the panel, trailing-update and inverse tile GEMMs of each phase are dealt
+// round-robin to the cluster's CTAs, and the phases are separated by cluster barriers (the tiles
+// live in global memory / L2; barrier.cluster release/acquire orders them).  Levels with few
+// segments (the serial base, narrow levels) use clusters so one block's tile work spreads over
+// several SMs instead of running serially in one CTA.
 __global__ void __launch_bounds__(BTHREADS) big_potrf_kernel(BigPotrfArgs g) {
   using S = FactorShape<64>;
   constexpr int LD = S::LD;
-  if (error_raised(g.err)) return;
-  const int k = blockIdx.x;
+  const int C = g.csize;
+  const int k = blockIdx.x / C, rank = blockIdx.x % C;
   int J;
+  // exits must be uniform over a cluster (cluster barriers follow): with csize > 1 a segment does
+  // not skip on another segment's error (its own step-(j-1) failure was already reported, and a
+  // later report can never supersede an earlier one)
+  if (C == 1 && error_raised(g.err)) return;
   if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, kActAll, J)) return;
   extern __shared__ __align__(16) double sm[];
-  double* DL = sm;             // 64 x LD diagonal tile
+  double* DL = sm;             // 64 x LD diagonal tile (rank 0)
   double* As = DL + BT * LD;   // two-stage staging of the tile GEMMs (4 * GSTAGE doubles)
   __shared__ int s_fail;
   double* D = const_cast<double*>(operand_ptr(g.D, g.seps, g.base_mode, k, g.j));
@@ -276,63 +291,90 @@ __global__ void __launch_bounds__(BTHREADS) big_potrf_kernel(BigPotrfArgs g) {
           dst[(size_t)r * ld + c] = addsrc ? addsrc[(size_t)r * ld + c] + v : v;
         }
   };
+  auto csync = [&]() {
+    if (C > 1) cluster_sync_all();
+    else __syncthreads();
+  };
   double acc[2][4][2];
   for (int kb = 0; kb < NB; ++kb) {
-    // diagonal tile -> DL, factor + invert (warps 0..3, named barrier 1)
-    __syncthreads();
-    for (int e = tid; e < BT * BT; e += BTHREADS) DL[(e / BT) * LD + e % BT] = D[(size_t)(kb * BT + e / BT) * n + kb * BT + e % BT];
-    __syncthreads();
-    int fail = 0;
-    if (warp < S::NWA) fail = potrf_trtri<64>(DL, &s_fail);
-    if (tid == 0) s_fail = fail;
-    __syncthreads();
-    if (s_fail) {
-      if (tid == 0) report_npd(g.err, g.level, g.j, k, kb * BT + s_fail);
+    // diagonal tile -> DL, factor + invert (rank 0, warps 0..3, named barrier 1)
+    if (rank == 0) {
+      __syncthreads();
+      for (int e = tid; e < BT * BT; e += BTHREADS) DL[(e / BT) * LD + e % BT] = D[(size_t)(kb * BT + e / BT) * n + kb * BT + e % BT];
+      __syncthreads();
+      int fail = 0;
+      if (warp < S::NWA) fail = potrf_trtri<64>(DL, &s_fail);
+      if (tid == 0) s_fail = fail;
+      __syncthreads();
+      if (s_fail) {
+        if (tid == 0) report_npd(g.err, g.level, g.j, k, kb * BT + s_fail);
+      } else {
+        // Linv_kk -> Li (full tile, zero upper); L_kk is not needed again
+        for (int e = tid; e < BT * BT; e += BTHREADS) {
+          const int r = e / BT, c = e % BT;
+          Li[(size_t)(kb * BT + r) * n + kb * BT + c] = c <= r ? DL[r * LD + c] : 0.0;
+        }
+      }
+    }
+    csync();
+    if (C > 1) {  // every rank learns the outcome from rank 0's shared memory
+      if (tid == 0) {
+        unsigned addr = (unsigned)__cvta_generic_to_shared(&s_fail), remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(addr));
+        int f;
+        asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(f) : "r"(remote) : "memory");
+        s_fail = f;
+      }
+      __syncthreads();
+      const int f = s_fail;
+      csync();  // rank 0's flag is not reused before everyone has read it
+      if (f) return;
+    } else if (s_fail) {
       return;
     }
-    // Linv_kk -> Li (full tile, zero upper); L_kk is not needed again
-    for (int e = tid; e < BT * BT; e += BTHREADS) {
-      const int r = e / BT, c = e % BT;
-      Li[(size_t)(kb * BT + r) * n + kb * BT + c] = c <= r ? DL[r * LD + c] : 0.0;
-    }
     // panel: L_ib = A_ib Linv_kk^T  (i > kb), in place in D
-    for (int ib = kb + 1; ib < NB; ++ib) {
+    for (int ib = kb + 1 + rank; ib < NB; ib += C) {
       gemm_tile_pipelined<false, true>(acc, D + (size_t)ib * BT * n + kb * BT, n, Li + (size_t)kb * BT * n + kb * BT, n, BT, BT, BT, 0, 0, 0, BT, As);
       __syncthreads();
       store_acc(D + (size_t)ib * BT * n + kb * BT, n, acc, 1.0, nullptr);
     }
-    __syncthreads();
-    // trailing: A_ij -= L_ib L_jb^T  (kb < jb <= ib)
+    csync();
+    // trailing: A_ij -= L_ib L_jb^T  (kb < jb <= ib), tiles dealt round-robin
+    int t = 0;
     for (int ib = kb + 1; ib < NB; ++ib)
-      for (int jb = kb + 1; jb <= ib; ++jb) {
+      for (int jb = kb + 1; jb <= ib; ++jb, ++t) {
+        if (t % C != rank) continue;
         gemm_tile_pipelined<false, true>(acc, D + (size_t)ib * BT * n + kb * BT, n, D + (size_t)jb * BT * n + kb * BT, n, BT, BT, BT, 0, 0, 0, BT, As);
         __syncthreads();
-        double* t = D + (size_t)ib * BT * n + jb * BT;
-        store_acc(t, n, acc, -1.0, t);
+        double* tt = D + (size_t)ib * BT * n + jb * BT;
+        store_acc(tt, n, acc, -1.0, tt);
       }
+    csync();
   }
-  __syncthreads();
   // inverse, block row by block row: Linv_ij = -Linv_ii sum_{m=j}^{i-1} L_im Linv_mj  (i > j)
   // T = sum_m L_im Linv_mj is formed in the (unused) strict upper tile D[j][i] as scratch.
   for (int ib = 1; ib < NB; ++ib) {
-    for (int jb = 0; jb < ib; ++jb) {
+    for (int jb = rank; jb < ib; jb += C) {
       // T = L[ib][jb..ib-1] * Linv[jb..ib-1][jb]   (k range (ib - jb) tiles)
       gemm_tile_pipelined<false, false>(acc, D + (size_t)ib * BT * n + jb * BT, n, Li + (size_t)jb * BT * n + jb * BT, n, BT, BT, (ib - jb) * BT, 0, 0, 0, (ib - jb) * BT, As);
       __syncthreads();
       store_acc(D + (size_t)jb * BT * n + ib * BT, n, acc, 1.0, nullptr);
     }
-    __syncthreads();
-    for (int jb = 0; jb < ib; ++jb) {
+    csync();
+    for (int jb = rank; jb < ib; jb += C) {
       gemm_tile_pipelined<false, false>(acc, Li + (size_t)ib * BT * n + ib * BT, n, D + (size_t)jb * BT * n + ib * BT, n, BT, BT, BT, 0, 0, 0, BT, As);
       __syncthreads();
       store_acc(Li + (size_t)ib * BT * n + jb * BT, n, acc, -1.0, nullptr);
     }
-    __syncthreads();
+    csync();
   }
   // zero the strict upper off-diagonal tiles of Linv
+  int t = 0;
   for (int ib = 0; ib < NB; ++ib)
-    for (int jb = ib + 1; jb < NB; ++jb)
+    for (int jb = ib + 1; jb < NB; ++jb, ++t) {
+      if (t % C != rank) continue;
       for (int e = tid; e < BT * BT; e += BTHREADS) Li[(size_t)(ib * BT + e / BT) * n + jb * BT + e % BT] = 0.0;
+    }
 }
 
 }  // namespace btd

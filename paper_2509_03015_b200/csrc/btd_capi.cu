@@ -437,6 +437,22 @@ cudaError_t big_copy(const BigCtx& c, int j, int act, btd::Operand src, btd::Ope
   return cudaGetLastError();
 }
 
+// CTAs per segment for big_potrf_kernel: 1 on wide levels; on narrow levels (the serial base, a
+// level with fewer segments than SMs) a cluster of up to 8 CTAs shares each block's tile GEMMs.
+// BTD_BIG_CLUSTER=<c> forces c (1 disables).
+int big_potrf_cluster(int K, int n, int sms) {
+  static int env = -2;
+  if (env == -2) {
+    const char* v = getenv("BTD_BIG_CLUSTER");
+    env = v ? std::max(1, std::min(8, atoi(v))) : -1;
+  }
+  const int NB = n / btd::BT;
+  const int maxc = std::max(1, std::min(8, NB * (NB - 1) / 2));  // more CTAs than trailing tiles idle
+  if (env > 0) return std::min(env, maxc);
+  if (K >= sms) return 1;
+  return std::max(1, std::min(maxc, sms / std::max(K, 1)));
+}
+
 // One level (coupled) or the base (base_mode) of the tiled factorization.
 cudaError_t big_factor_level(const BigCtx& c, int level, int Jmax, int n, const double* diag, const double* sub,
                              double* Linv, double* Lsub, double* Sl, double* Sr, double* Ssub, char* ws,
@@ -447,7 +463,7 @@ cudaError_t big_factor_level(const BigCtx& c, int level, int Jmax, int n, const 
   double* WX = WD + (size_t)c.K * nn;
   double* WP = WX + (size_t)c.K * 2 * nn;
   const bool coupled = !c.base_mode;
-  const Operand oWD = opnd(WD, nn, n, kIdxSeg), oWX = opnd(WX, 2 * nn, n, kIdxSeg), oWP = opnd(WP, 2 * nn, n, kIdxSeg);
+  const Operand oWD = opnd(WD, nn, n, kIdxSeg), oWP = opnd(WP, 2 * nn, n, kIdxSeg);
   const Operand oWXhi = opnd(WX, 2 * nn, n, kIdxSeg, 0, n), oWPhi = opnd(WP, 2 * nn, n, kIdxSeg, 0, n);
   const Operand oLinv = opnd(Linv, nn, n, kIdxSegRow);
   cudaError_t e;
@@ -457,16 +473,16 @@ cudaError_t big_factor_level(const BigCtx& c, int level, int Jmax, int n, const 
     if (e != cudaSuccess) return e; \
   } while (0)
   // ---- prologue ----
+  // X1 (A_{j+1,j}, or C_R at the last row) is read by the P1 product straight from `sub`; only the
+  // fill coupling Gt lives in the workspace (rows n..2n of WX)
   BIG_CHECK(big_copy(c, 0, kActAll, opnd(diag, nn, n, kIdxSegRow), oWD, n, n));
   if (coupled) {
-    BIG_CHECK(big_copy(c, 0, kActNotLast, opnd(sub, nn, n, kIdxSegRow), oWX, n, n));
-    BIG_CHECK(big_copy(c, 0, kActLast, opnd(sub, nn, n, kIdxSegStop, -1), oWX, n, n));
     BIG_CHECK(big_copy(c, 0, kActAll, opnd(sub, nn, n, kIdxSegStart, 0, 0, 1), oWXhi, n, n));  // C_L^T
     BIG_CHECK(big_copy(c, 0, kActAll, opnd(sub, nn, n, kIdxSegStart), opnd(Lsub, nn, n, kIdxSegStart), n, n));
     BIG_CHECK(big_copy(c, 0, kActAll, opnd(sub, nn, n, kIdxSegStop, -1), opnd(Lsub, nn, n, kIdxSegStop, -1), n, n));
-  } else if (c.N > 1) {
-    BIG_CHECK(big_copy(c, 0, kActNotLast, opnd(sub, nn, n, kIdxSegRow), oWX, n, n));
   }
+  const Operand oLinvT = opnd(Linv, nn, n, kIdxSegRow, 0, 0, 1);
+  const Operand oL1 = opnd(Lsub, nn, n, kIdxSegRow), oL1t = opnd(Lsub, nn, n, kIdxSegRow, 0, 0, 1);
   for (int j = 0; j < Jmax; ++j) {
     {
       BigPotrfArgs a{};
@@ -481,20 +497,40 @@ cudaError_t big_factor_level(const BigCtx& c, int level, int Jmax, int n, const 
       a.err = err;
       const int smem = (BT * FactorShape<64>::LD + 4 * GSTAGE) * (int)sizeof(double);
       static bool conf = false;
+      static int sms = 0;
       if (!conf) {
         BIG_CHECK(cudaFuncSetAttribute(big_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        BIG_CHECK(cudaFuncSetAttribute(big_potrf_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         conf = true;
       }
-      big_potrf_kernel<<<(unsigned)c.K, BTHREADS, smem, c.s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
-      BIG_CHECK(cudaGetLastError());
+      // a cluster of CTAs per segment when the level is too narrow to fill the SMs
+      a.csize = big_potrf_cluster(c.K, n, sms);
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3((unsigned)(c.K * a.csize));
+      cfg.blockDim = dim3(BTHREADS);
+      cfg.dynamicSmemBytes = (size_t)smem;
+      cfg.stream = c.s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = (unsigned)a.csize;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      BIG_CHECK(cudaLaunchKernelEx(&cfg, big_potrf_kernel, a)); g_launches.fetch_add(1, std::memory_order_relaxed);
     }
-    // Pt = Xt Linv^T
-    BIG_CHECK(big_gemm(c, j, coupled ? kActAll : kActNotLast, oWX, opnd(Linv, nn, n, kIdxSegRow, 0, 0, 1), oWP, oWP,
-                       coupled ? 2 * n : n, n, n, 1.0, 0.0, 0, 1));
+    // P1 = X1 Linv^T: inside the segment it is L_{j+1,j}, written straight into the hierarchy's Lsub
+    // slot; at the last row it is Y_R = C_R Linv^T (workspace WP).  P2 = Gt Linv^T -> WP rows n..2n.
+    BIG_CHECK(big_gemm(c, j, kActNotLast, opnd(sub, nn, n, kIdxSegRow), oLinvT, oL1, oL1, n, n, n, 1.0, 0.0, 0, 1));
     if (coupled) {
+      BIG_CHECK(big_gemm(c, j, kActLast, opnd(sub, nn, n, kIdxSegStop, -1), oLinvT, oWP, oWP, n, n, n, 1.0, 0.0, 0, 1));
+      BIG_CHECK(big_gemm(c, j, kActAll, oWXhi, oLinvT, oWPhi, oWPhi, n, n, n, 1.0, 0.0, 0, 1));
       // fill block G^T = -P2 P1^T, or at the last row S_sub = (-P2 P1^T)^T
       const Operand oP1t = opnd(WP, 2 * nn, n, kIdxSeg, 0, 0, 1);
-      BIG_CHECK(big_gemm(c, j, kActNotLast, oWPhi, oP1t, oWXhi, oWXhi, n, n, n, -1.0, 0.0));
+      BIG_CHECK(big_gemm(c, j, kActNotLast, oWPhi, oL1t, oWXhi, oWXhi, n, n, n, -1.0, 0.0));
       BIG_CHECK(big_gemm(c, j, kActLast, oWPhi, oP1t, opnd(Ssub, nn, n, kIdxSeg), opnd(Ssub, nn, n, kIdxSeg), n, n, n,
                          -1.0, 0.0, 0, 0, 1));
       // S_L (+)= P2 P2^T
@@ -505,12 +541,8 @@ cudaError_t big_factor_level(const BigCtx& c, int level, int Jmax, int n, const 
       BIG_CHECK(big_gemm(c, j, kActLast, oWP, oP1t, opnd(Sr, nn, n, kIdxSeg), opnd(Sr, nn, n, kIdxSeg), n, n, n, 1.0,
                          0.0, 1));
     }
-    // D_{j+1} = A_{j+1,j+1} - P1 P1^T ; L_{j+1,j} -> hierarchy ; next X1
-    BIG_CHECK(big_gemm(c, j, kActNotLast, oWP, opnd(WP, 2 * nn, n, kIdxSeg, 0, 0, 1), opnd(diag, nn, n, kIdxSegRow, 1),
-                       oWD, n, n, n, -1.0, 1.0, 1));
-    BIG_CHECK(big_copy(c, j, kActNotLast, oWP, opnd(Lsub, nn, n, kIdxSegRow), n, n));
-    BIG_CHECK(big_copy(c, j, kActBeforeSecondLast, opnd(sub, nn, n, kIdxSegRow, 1), oWX, n, n));
-    if (coupled) BIG_CHECK(big_copy(c, j, kActSecondLast, opnd(sub, nn, n, kIdxSegStop, -1), oWX, n, n));
+    // D_{j+1} = A_{j+1,j+1} - P1 P1^T
+    BIG_CHECK(big_gemm(c, j, kActNotLast, oL1, oL1t, opnd(diag, nn, n, kIdxSegRow, 1), oWD, n, n, n, -1.0, 1.0, 1));
   }
   return cudaSuccess;
 }
