@@ -74,6 +74,7 @@ struct GemmArgs {
                          // 3: op(A)[r][k] == 0 for k < r (A = L^T)
   int store_trans;       // write Cout^T
   int tiles_n;
+  int k0;                // first segment of this launch (blockIdx.y = k - k0)
   const DevErr* err;
 };
 
@@ -173,7 +174,7 @@ __device__ __forceinline__ void gemm_tile_pipelined(double (&acc)[2][4][2], cons
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(BTHREADS) bt_gemm_kernel(GemmArgs g) {
   if (error_raised(g.err)) return;
-  const int k = blockIdx.y;
+  const int k = g.k0 + blockIdx.y;
   int J;
   if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, g.act, J)) return;
   const int tm = blockIdx.x / g.tiles_n, tn = blockIdx.x % g.tiles_n;
@@ -218,13 +219,14 @@ struct CopyArgs {
   long long N;
   int base_mode, j, act;
   int rows, cols;  // of the destination
+  int k0;          // first segment of this launch
   const DevErr* err;
 };
 
 // dst[r][c] = src[r][c] (or src[c][r] when src.trans); blockIdx.y = segment
 __global__ void bt_copy_kernel(CopyArgs c) {
   if (error_raised(c.err)) return;
-  const int k = blockIdx.y;
+  const int k = c.k0 + blockIdx.y;
   int J;
   if (!segment_active(c.seps, c.base_mode, c.N, k, c.j, c.act, J)) return;
   const double* s = operand_ptr(c.src, c.seps, c.base_mode, k, c.j);
@@ -245,6 +247,7 @@ struct BigPotrfArgs {
   long long N;
   int base_mode, j, n, level;
   int csize;     // CTAs per segment (a thread-block cluster when > 1)
+  int k0;        // first segment of this launch
   DevErr* err;
 };
 
@@ -263,7 +266,7 @@ __global__ void __launch_bounds__(BTHREADS) big_potrf_kernel(BigPotrfArgs g) {
   using S = FactorShape<64>;
   constexpr int LD = S::LD;
   const int C = g.csize;
-  const int k = blockIdx.x / C, rank = blockIdx.x % C;
+  const int k = g.k0 + blockIdx.x / C, rank = blockIdx.x % C;
   int J;
   // exits must be uniform over a cluster (cluster barriers follow): with csize > 1 a segment does
   // not skip on another segment's error (its own step-(j-1) failure was already reported, and a

@@ -72,9 +72,16 @@ struct btd_hierarchy {
   std::vector<cudaEvent_t> ev;
   int nev = 0;
   cudaStream_t copy_stream = nullptr;  // btd_factorize_from_host
+  // n > 64: wide levels run as two half-level launch sequences on two streams, so one half's
+  // Cholesky kernels overlap the other half's tile GEMMs
+  cudaStream_t aux_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   ~btd_hierarchy() {
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (aux_stream) cudaStreamDestroy(aux_stream);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
   }
 };
 
@@ -371,9 +378,11 @@ btd::Operand opnd(const double* base, long long stride, int ld, int index, int d
 struct BigCtx {
   const int* seps;
   long long N;
-  int base_mode, K;
+  int base_mode, K;  // K: segments of this launch sequence, starting at segment k0
   const btd::DevErr* err;
   cudaStream_t s;
+  int k0 = 0;
+  int Kws = 0;  // segments the per-segment workspaces are laid out for (0: K)
 };
 
 cudaError_t big_gemm(const BigCtx& c, int j, int act, btd::Operand A, btd::Operand B, btd::Operand Cin,
@@ -409,6 +418,7 @@ cudaError_t big_gemm(const BigCtx& c, int j, int act, btd::Operand A, btd::Opera
   g.tri = tri;
   g.store_trans = store_trans;
   g.tiles_n = (n + btd::BT - 1) / btd::BT;
+  g.k0 = c.k0;
   g.err = c.err;
   dim3 grid((unsigned)(((m + btd::BT - 1) / btd::BT) * g.tiles_n), (unsigned)c.K);
   if (!A.trans && !B.trans) btd::bt_gemm_kernel<false, false><<<grid, btd::BTHREADS, smem, c.s>>>(g);
@@ -430,6 +440,7 @@ cudaError_t big_copy(const BigCtx& c, int j, int act, btd::Operand src, btd::Ope
   a.act = act;
   a.rows = rows;
   a.cols = cols;
+  a.k0 = c.k0;
   a.err = c.err;
   const long long tot = (long long)rows * cols;
   dim3 grid((unsigned)std::min<long long>((tot + 255) / 256, 64), (unsigned)c.K);
@@ -453,15 +464,39 @@ int big_potrf_cluster(int K, int n, int sms) {
   return std::max(1, std::min(maxc, sms / std::max(K, 1)));
 }
 
+// Split a wide n > 64 level into two half-level launch sequences on two streams (BTD_BIG_SPLIT=0
+// disables): each half's big_potrf_kernel (latency-bound, < 2 waves) overlaps the other half's
+// tile GEMMs.
+bool big_split_level(int64_t K) {
+  static int env = -1, sms = 0;
+  if (env < 0) {
+    const char* v = getenv("BTD_BIG_SPLIT");
+    env = (v && v[0] == '0') ? 0 : 1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return env == 1 && K >= 2 * (int64_t)sms;
+}
+
+cudaError_t ensure_aux(btd_hierarchy* h) {
+  cudaError_t e = cudaSuccess;
+  if (!h->aux_stream) e = cudaStreamCreateWithFlags(&h->aux_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess && !h->ev_fork) e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess && !h->ev_join) e = cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
+  return e;
+}
+
 // One level (coupled) or the base (base_mode) of the tiled factorization.
 cudaError_t big_factor_level(const BigCtx& c, int level, int Jmax, int n, const double* diag, const double* sub,
                              double* Linv, double* Lsub, double* Sl, double* Sr, double* Ssub, char* ws,
                              btd::DevErr* err) {
   using namespace btd;
   const long long nn = (long long)n * n;
+  const size_t Kws = (size_t)(c.Kws ? c.Kws : c.K);  // the same layout for both halves of a split level
   double* WD = (double*)ws;
-  double* WX = WD + (size_t)c.K * nn;
-  double* WP = WX + (size_t)c.K * 2 * nn;
+  double* WX = WD + Kws * nn;
+  double* WP = WX + Kws * 2 * nn;
   const bool coupled = !c.base_mode;
   const Operand oWD = opnd(WD, nn, n, kIdxSeg), oWP = opnd(WP, 2 * nn, n, kIdxSeg);
   const Operand oWXhi = opnd(WX, 2 * nn, n, kIdxSeg, 0, n), oWPhi = opnd(WP, 2 * nn, n, kIdxSeg, 0, n);
@@ -494,6 +529,7 @@ cudaError_t big_factor_level(const BigCtx& c, int level, int Jmax, int n, const 
       a.j = j;
       a.n = n;
       a.level = level;
+      a.k0 = c.k0;
       a.err = err;
       const int smem = (BT * FactorShape<64>::LD + 4 * GSTAGE) * (int)sizeof(double);
       static bool conf = false;
@@ -1001,9 +1037,28 @@ static int enqueue_factor(btd_hierarchy* h, const double* diag, const double* su
       BigCtx c{(const int*)(pers + lp.off_seps), lp.N, 0, (int)lp.K, err, stream};
       double* next_diag = (double*)(scr + lp.off_next_diag);
       prof_mark(h, stream);
-      e = big_factor_level(c, (int)l, jmax, n, cd, cs, (double*)(pers + lp.off_linv), (double*)(pers + lp.off_lsub),
-                           next_diag, (double*)(scr + lp.off_sr), (double*)(scr + lp.off_next_sub),
-                           scr + h->off_big_ws, err);
+      auto level_seq = [&](const BigCtx& cc) {
+        return big_factor_level(cc, (int)l, jmax, n, cd, cs, (double*)(pers + lp.off_linv),
+                                (double*)(pers + lp.off_lsub), next_diag, (double*)(scr + lp.off_sr),
+                                (double*)(scr + lp.off_next_sub), scr + h->off_big_ws, err);
+      };
+      if (big_split_level(lp.K)) {
+        e = ensure_aux(h);
+        if (e == cudaSuccess) e = cudaEventRecord(h->ev_fork, stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(h->aux_stream, h->ev_fork, 0);
+        BigCtx ca = c, cb = c;
+        ca.Kws = cb.Kws = (int)lp.K;
+        ca.K = (int)(lp.K / 2);
+        cb.k0 = ca.K;
+        cb.K = (int)lp.K - ca.K;
+        cb.s = h->aux_stream;
+        if (e == cudaSuccess) e = level_seq(ca);
+        if (e == cudaSuccess) e = level_seq(cb);
+        if (e == cudaSuccess) e = cudaEventRecord(h->ev_join, h->aux_stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, h->ev_join, 0);
+      } else {
+        e = level_seq(c);
+      }
       prof_mark(h, stream);
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(big level)");
       btd::assemble_schur_diag_kernel<<<flat_grid(lp.P * h->n * h->n), 256, 0, stream>>>(
