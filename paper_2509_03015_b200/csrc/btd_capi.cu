@@ -945,6 +945,41 @@ struct HostSrc {
   double* dev_sub;
 };
 
+// H2D of diagonal blocks [b0, b0 + nb) from pinned host memory.  Every kernel reads only the lower
+// triangle of a diagonal block (potrf, the D / S_L updates and the Schur assembly), so for n >= 32
+// the rows are sent in G bands: band g (rows [g n/G, (g+1) n/G)) only its first (g+1) n/G columns,
+// the last band in full (G = 4 for n >= 64: 5/8 of the bytes; G = 2 for n >= 32: 3/4), one pitched
+// 3D copy per band with rows of >= 128 bytes.  The device copy's remaining upper triangle is never
+// read.  BTD_H2D_LOWER=0 sends whole blocks, BTD_H2D_LOWER=<G> forces G bands.
+cudaError_t copy_diag_h2d(double* dev, const double* host, int64_t b0, int64_t nb, int64_t n, cudaStream_t s) {
+  static int env = -1;
+  if (env < 0) {
+    const char* v = getenv("BTD_H2D_LOWER");
+    env = v ? atoi(v) : 99;
+  }
+  const size_t nn = (size_t)n * n;
+  if (nb <= 0) return cudaSuccess;
+  int G = n >= 64 ? 4 : n >= 32 ? 2 : 1;
+  if (env != 99) G = env <= 0 ? 1 : std::min<int>(env, G);
+  while (G > 1 && n % G) --G;
+  if (G <= 1)
+    return cudaMemcpyAsync(dev + b0 * nn, host + b0 * nn, (size_t)nb * nn * sizeof(double), cudaMemcpyHostToDevice, s);
+  const size_t pitch = (size_t)n * sizeof(double);
+  const int64_t band = n / G;
+  for (int g = 0; g < G; ++g) {
+    cudaMemcpy3DParms p{};
+    p.srcPtr = make_cudaPitchedPtr(const_cast<double*>(host), pitch, (size_t)n, (size_t)n);
+    p.dstPtr = make_cudaPitchedPtr(dev, pitch, (size_t)n, (size_t)n);
+    p.srcPos = make_cudaPos(0, (size_t)(g * band), (size_t)b0);
+    p.dstPos = p.srcPos;
+    p.extent = make_cudaExtent((size_t)((g + 1) * band) * sizeof(double), (size_t)band, (size_t)nb);
+    p.kind = cudaMemcpyHostToDevice;
+    cudaError_t e = cudaMemcpy3DAsync(&p, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t chunked_level0(btd_hierarchy* h, btd::FactorArgs a, const LevelPlan& lp, const HostSrc& src,
                            cudaStream_t stream) {
   if (!h->copy_stream) {
@@ -969,8 +1004,7 @@ cudaError_t chunked_level0(btd_hierarchy* h, btd::FactorArgs a, const LevelPlan&
     // segments [ka, kb) read diag/sub rows up to seps[kb] (exclusive for sub, inclusive for the
     // separator diag read by the assembly); the last chunk takes everything that is left
     const int64_t row1 = (c + 1 == chunks) ? lp.N : lp.sep(kb) + 1;
-    e = cudaMemcpyAsync(src.dev_diag + row0 * nn, src.diag + row0 * nn, (size_t)(row1 - row0) * nn * sizeof(double),
-                        cudaMemcpyHostToDevice, h->copy_stream);
+    e = copy_diag_h2d(src.dev_diag, src.diag, row0, row1 - row0, h->n, h->copy_stream);
     const int64_t srow1 = std::min<int64_t>(row1, lp.N - 1);
     if (e == cudaSuccess && srow1 > row0)
       e = cudaMemcpyAsync(src.dev_sub + row0 * nn, src.sub + row0 * nn, (size_t)(srow1 - row0) * nn * sizeof(double),
@@ -1021,7 +1055,7 @@ static int enqueue_factor(btd_hierarchy* h, const double* diag, const double* su
 
   if (host && (h->big || h->levels.empty())) {  // no chunking: one bulk copy, then the usual path
     const size_t nn = (size_t)h->n * h->n * sizeof(double);
-    e = cudaMemcpyAsync(host->dev_diag, host->diag, (size_t)h->N * nn, cudaMemcpyHostToDevice, stream);
+    e = copy_diag_h2d(host->dev_diag, host->diag, 0, h->N, h->n, stream);
     if (e == cudaSuccess && h->N > 1)
       e = cudaMemcpyAsync(host->dev_sub, host->sub, (size_t)(h->N - 1) * nn, cudaMemcpyHostToDevice, stream);
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize_from_host(copy)");
