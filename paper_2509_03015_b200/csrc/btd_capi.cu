@@ -76,7 +76,10 @@ struct btd_hierarchy {
   // Cholesky kernels overlap the other half's tile GEMMs
   cudaStream_t aux_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_half[2] = {nullptr, nullptr};  // host input: the two halves' H2D copies landed
   ~btd_hierarchy() {
+    for (cudaEvent_t e : ev_half)
+      if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (aux_stream) cudaStreamDestroy(aux_stream);
@@ -1053,7 +1056,31 @@ static int enqueue_factor(btd_hierarchy* h, const double* diag, const double* su
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(seps)");
 
-  if (host && (h->big || h->levels.empty())) {  // no chunking: one bulk copy, then the usual path
+  // n > 64 with a split level 0: each half's rows are copied on the copy stream and the half's
+  // launch sequence starts as soon as they have landed (half A computes while half B copies)
+  const bool big_overlap = host && h->big && !h->levels.empty() && big_split_level(h->levels[0].K);
+  if (big_overlap) {
+    const LevelPlan& lp = h->levels[0];
+    const size_t nn = (size_t)h->n * h->n;
+    e = ensure_aux(h);
+    if (e == cudaSuccess && !h->copy_stream) e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i)
+      if (!h->ev_half[i]) e = cudaEventCreateWithFlags(&h->ev_half[i], cudaEventDisableTiming);
+    // the copy stream must not overwrite buffers earlier work on `stream` still reads
+    if (e == cudaSuccess) e = cudaEventRecord(h->ev_fork, stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->copy_stream, h->ev_fork, 0);
+    const int64_t rows[3] = {0, lp.sep(lp.K / 2) + 1, h->N};
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      e = copy_diag_h2d(host->dev_diag, host->diag, rows[i], rows[i + 1] - rows[i], h->n, h->copy_stream);
+      const int64_t s1 = std::min<int64_t>(rows[i + 1], h->N - 1);
+      if (e == cudaSuccess && s1 > rows[i])
+        e = cudaMemcpyAsync(host->dev_sub + rows[i] * nn, host->sub + rows[i] * nn, (size_t)(s1 - rows[i]) * nn * sizeof(double),
+                            cudaMemcpyHostToDevice, h->copy_stream);
+      if (e == cudaSuccess) e = cudaEventRecord(h->ev_half[i], h->copy_stream);
+    }
+    if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize_from_host(copy)");
+    host = nullptr;
+  } else if (host && (h->big || h->levels.empty())) {  // no chunking: one bulk copy, then the usual path
     const size_t nn = (size_t)h->n * h->n * sizeof(double);
     e = copy_diag_h2d(host->dev_diag, host->diag, 0, h->N, h->n, stream);
     if (e == cudaSuccess && h->N > 1)
@@ -1080,6 +1107,10 @@ static int enqueue_factor(btd_hierarchy* h, const double* diag, const double* su
         e = ensure_aux(h);
         if (e == cudaSuccess) e = cudaEventRecord(h->ev_fork, stream);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(h->aux_stream, h->ev_fork, 0);
+        if (l == 0 && big_overlap) {  // each half waits for its own rows only
+          if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, h->ev_half[0], 0);
+          if (e == cudaSuccess) e = cudaStreamWaitEvent(h->aux_stream, h->ev_half[1], 0);
+        }
         BigCtx ca = c, cb = c;
         ca.Kws = cb.Kws = (int)lp.K;
         ca.K = (int)(lp.K / 2);

@@ -160,7 +160,7 @@ def test_sharded_gpu_matches_unsharded(case):
     assert rres <= REL_RES
 
 
-@pytest.mark.parametrize("N,n,d", [(4096, 64, 1), (20000, 8, 2), (3000, 33, 1), (600, 128, 2)])
+@pytest.mark.parametrize("N,n,d", [(4096, 64, 1), (20000, 8, 2), (3000, 33, 1), (600, 128, 2), (2800, 128, 1)])
 def test_host_input_overlapped_copy_is_bitwise_device_path(N, n, d):
     """btd_factorize_from_host (chunked H2D overlapping the level-0 kernels) == device-input path."""
     A, B = pkg.generate_spd_btd(N, n, d, seed=11)
