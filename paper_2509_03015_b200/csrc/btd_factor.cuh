@@ -668,6 +668,54 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
       cp_async_commit();
     }
     // D_{j+1} = A_{j+1,j+1} - P1^T P1  (or S_R at the last row of a coupled segment)
+#ifndef BTD_D16
+    if constexpr (NT == 64) {
+      // 36 lower 8x8 tiles balanced over the 8 warps (4-5 each, max 5 DMMAs per k step instead of
+      // 8 for the warps that held two 16x16 tiles): warps 2p, 2p+1 share the tile rows 7-p and p,
+      // (7-p, 0..7-p) then (p, 0..p), split 5 / 4.
+      const int pr = warp >> 1, first = (warp & 1) * 5;
+      double dacc[5][2];
+      int dtr[5], dtc[5];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        const int idx = first + i;
+        const bool hi = idx <= 7 - pr;
+        dtr[i] = idx < 9 ? (hi ? 7 - pr : pr) : -1;
+        dtc[i] = hi ? idx : idx - (8 - pr);
+        dacc[i][0] = dacc[i][1] = 0.0;
+      }
+      const double* base = XP + (lane >> 2) * LD + (lane & 3);
+#pragma unroll 4
+      for (int k0 = 0; k0 < NT; k0 += 4) {
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+          if (dtr[i] < 0) continue;
+          dmma(dacc[i], base[dtr[i] * 8 * LD + k0], base[dtc[i] * 8 * LD + k0]);
+        }
+      }
+      cp_async_wait_all();
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        if (dtr[i] < 0) continue;
+        const int r = dtr[i] * 8 + (lane >> 2), c = dtc[i] * 8 + 2 * (lane & 3);
+        if (!last) {
+          double2* dst = reinterpret_cast<double2*>(DL + r * LD + c);
+          double2 v = *dst;
+          v.x = (r == c && r >= n) ? 1.0 : v.x - dacc[i][0];
+          v.y = (r == c + 1 && r >= n) ? 1.0 : v.y - dacc[i][1];
+          *dst = v;
+        } else if (r < n) {
+          double* dst = args.Sr + (size_t)k * bs + (size_t)r * n;
+          if (c < n) dst[c] = dacc[i][0];
+          if (c + 1 < n) dst[c + 1] = dacc[i][1];
+        }
+      }
+      __syncthreads();
+      BTD_PHASE(3);
+      continue;
+    }
+#endif
     double acc[S::MAXD][SUB][SUB][2];
     int drr[S::MAXD], dcc[S::MAXD];
 #pragma unroll
