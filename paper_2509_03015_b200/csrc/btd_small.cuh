@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(kSmallThreads, 3) factor_small_kernel(FactorAr
 // one 8-lane group per segment, DC right-hand-side columns per pass (grid.y covers d).
 // z_j is parked in x (down: scratch; up/base: overwritten by w_j in the backward sweep).
 // ============================================================================================
+// (register caps for more resident CTAs were measured slower: they spill the prefetched operands)
 template <int DC>
 __global__ void __launch_bounds__(kSmallThreads) solve_small_kernel(SolveArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -225,11 +226,21 @@ __global__ void __launch_bounds__(kSmallThreads) solve_small_kernel(SolveArgs a)
     for (int c = 0; c < DC; ++c)
       if (c0 + c < d) p[(size_t)r * d + c0 + c] = v[c];
   };
-  // y = M v (row r of M) or M^T v (column r of M); v broadcast inside the group
-  auto mv = [&](const double* M, bool trans, const double (&v)[DC], double (&y)[DC], double sign, bool ok) {
-    double m8[8];
+  // operand rows of one step, loaded a step ahead of their use (the sweeps are memory-latency
+  // bound: 8-lane groups, a few hundred cycles of shuffles per step against ~1 us of DRAM latency)
+  auto ld_full = [&](const double* M, bool trans, double (&m8)[8], bool ok) {  // row r of M or M^T
 #pragma unroll
     for (int q = 0; q < 8; ++q) m8[q] = (ok && rv && q < n) ? (trans ? M[(size_t)q * n + r] : M[(size_t)r * n + q]) : 0.0;
+  };
+  auto ld_pack = [&](const double* P, bool trans, double (&m8)[8], bool ok) {  // row r of Linv or Linv^T
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const bool in = ok && rv && q < n && (trans ? q >= r : q <= r);
+      m8[q] = in ? (trans ? P[packed_offset_(q) + r] : P[packed_offset_(r) + q]) : 0.0;
+    }
+  };
+  // y (+)= sign * m8 . v  (v broadcast inside the group)
+  auto dot = [&](const double (&m8)[8], const double (&v)[DC], double (&y)[DC], double sign) {
 #pragma unroll
     for (int c = 0; c < DC; ++c) {
       double s = 0.0;
@@ -238,21 +249,10 @@ __global__ void __launch_bounds__(kSmallThreads) solve_small_kernel(SolveArgs a)
       y[c] = fma(sign, s, y[c]);
     }
   };
-  // y = Linv t (packed row r) or Linv^T t (packed column r)
-  auto mv_pack = [&](const double* P, bool trans, const double (&t)[DC], double (&y)[DC], bool ok) {
+  auto mv = [&](const double* M, bool trans, const double (&v)[DC], double (&y)[DC], double sign, bool ok) {
     double m8[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const bool in = ok && rv && q < n && (trans ? q >= r : q <= r);
-      m8[q] = in ? (trans ? P[packed_offset_(q) + r] : P[packed_offset_(r) + q]) : 0.0;
-    }
-#pragma unroll
-    for (int c = 0; c < DC; ++c) {
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) s = fma(m8[q], gbc(t[c], q), s);
-      if (ok) y[c] = s;  // inactive iterations (shorter segments of the warp) keep y
-    }
+    ld_full(M, trans, m8, ok);
+    dot(m8, v, y, sign);
   };
 
   double corr0[DC], corr1[DC], xs0[DC], xs1[DC];
@@ -270,11 +270,23 @@ __global__ void __launch_bounds__(kSmallThreads) solve_small_kernel(SolveArgs a)
   double z[DC];
 #pragma unroll
   for (int c = 0; c < DC; ++c) z[c] = 0.0;
+  double fL[8], fP[8], fb[DC];  // step j's operands (prefetched)
+  auto ld_fwd = [&](int j, double (&L)[8], double (&P)[8], double (&b)[DC]) {
+    const bool act = valid && j < J;
+    const long long row = start + j;
+    ld_full(act && j > 0 ? a.Lsub + (row - 1) * bs : nullptr, false, L, act && j > 0);
+    ld_pack(act ? a.Linv + row * (size_t)pk : nullptr, false, P, act);
+    ld_vec(act ? a.rhs + row * ps : nullptr, b);
+  };
+  ld_fwd(0, fL, fP, fb);
   for (int j = 0; j < jw; ++j) {
     const bool act = valid && j < J;
     const long long row = start + j;
+    double nL[8], nP[8], nb[DC];
+    ld_fwd(j + 1, nL, nP, nb);
     double t[DC];
-    ld_vec(act ? a.rhs + row * ps : nullptr, t);
+#pragma unroll
+    for (int c = 0; c < DC; ++c) t[c] = fb[c];
     if (act && j == 0) {
 #pragma unroll
       for (int c = 0; c < DC; ++c) t[c] -= corr0[c];
@@ -283,28 +295,70 @@ __global__ void __launch_bounds__(kSmallThreads) solve_small_kernel(SolveArgs a)
 #pragma unroll
       for (int c = 0; c < DC; ++c) t[c] -= corr1[c];
     }
-    mv(act && j > 0 ? a.Lsub + (row - 1) * bs : nullptr, false, z, t, -1.0, act && j > 0);
-    mv_pack(act ? a.Linv + row * (size_t)pk : nullptr, false, t, z, act);
+    dot(fL, z, t, -1.0);  // fL is zero at j == 0
+    double zn[DC];
+#pragma unroll
+    for (int c = 0; c < DC; ++c) zn[c] = 0.0;
+    dot(fP, t, zn, 1.0);
+    if (act) {
+#pragma unroll
+      for (int c = 0; c < DC; ++c) z[c] = zn[c];  // inactive iterations (shorter segments of the warp) keep z
+    }
     st_vec(act ? a.x + row * ps : nullptr, z, act);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      fL[q] = nL[q];
+      fP[q] = nP[q];
+    }
+#pragma unroll
+    for (int c = 0; c < DC; ++c) fb[c] = nb[c];
   }
   // ---- backward sweep: w_j = Linv_j^T (z_j - L_{j+1,j}^T w_{j+1}) ----
+  // group-local index: the groups run their own j = J-1 .. 0 in the same iterations
   double w[DC], w_last[DC];
 #pragma unroll
   for (int c = 0; c < DC; ++c) w[c] = w_last[c] = 0.0;
+  auto ld_bwd = [&](int jj, double (&L)[8], double (&P)[8], double (&zz)[DC]) {
+    const int j = jj - (jw - J);
+    const bool act = valid && j >= 0 && jj >= 0;
+    const long long row = start + (act ? j : 0);
+    ld_full(act && j < J - 1 ? a.Lsub + row * bs : nullptr, true, L, act && j < J - 1);
+    ld_pack(act ? a.Linv + row * (size_t)pk : nullptr, true, P, act);
+    ld_vec(act ? a.x + row * ps : nullptr, zz);
+  };
+  __syncwarp();  // this lane's z_j stores (forward) are read back by the same lane only
+  double bL[8], bP[8], bz[DC];
+  ld_bwd(jw - 1, bL, bP, bz);
   for (int jj = jw - 1; jj >= 0; --jj) {
-    // group-local index: the groups run their own j = J-1 .. 0 in the same iterations
     const int j = jj - (jw - J);
     const bool act = valid && j >= 0;
     const long long row = start + (act ? j : 0);
+    double nL[8], nP[8], nz[DC];
+    ld_bwd(jj - 1, nL, nP, nz);
     double t[DC];
-    ld_vec(act ? a.x + row * ps : nullptr, t);
-    mv(act && j < J - 1 ? a.Lsub + row * bs : nullptr, true, w, t, -1.0, act && j < J - 1);
-    mv_pack(act ? a.Linv + row * (size_t)pk : nullptr, true, t, w, act);
+#pragma unroll
+    for (int c = 0; c < DC; ++c) t[c] = bz[c];
+    dot(bL, w, t, -1.0);  // bL is zero at j == J - 1
+    double wn[DC];
+#pragma unroll
+    for (int c = 0; c < DC; ++c) wn[c] = 0.0;
+    dot(bP, t, wn, 1.0);
+    if (act) {
+#pragma unroll
+      for (int c = 0; c < DC; ++c) w[c] = wn[c];
+    }
     if (mode != kSolveDown) st_vec(act ? a.x + row * ps : nullptr, w, act);
     if (act && j == J - 1) {
 #pragma unroll
       for (int c = 0; c < DC; ++c) w_last[c] = w[c];
     }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      bL[q] = nL[q];
+      bP[q] = nP[q];
+    }
+#pragma unroll
+    for (int c = 0; c < DC; ++c) bz[c] = nz[c];
   }
   if (mode == kSolveDown) {  // fold: f_R = C_R w_last ; f_L = C_L^T w_0
     double fr[DC], fl[DC];
