@@ -12,7 +12,8 @@ from .errors import (BadMagic, BtdFormatError, IoError, TruncatedPayload, Versio
 from .schur import (FactorLevel, RecursionConfig, level_factor, plan_partition, recursive_factorize,
                     recursive_solve)
 from .synthgen import generate_spd_btd
-from .report import residual_report, btd_matmul
+from .report import (SWEEPS, BenchRow, bench_sweep, btd_matmul, device_bytes, format_table, parse_sweep,
+                     residual_report, time_call)
 from .kalman import StateSpaceModel, build_normal_equations, generate_rotation_model
 from .btdfile import read_btd, write_btd
 
@@ -26,4 +27,5 @@ __all__ = [
     "NotPositiveDefinite", "PartitionPlan", "RecursionConfig", "SingularDiagonal", "btd_matmul",
     "check_conformal", "generate_spd_btd", "level_factor", "new_btd", "new_rhs", "plan_partition",
     "recursive_factorize", "recursive_solve", "residual_report",
+    "SWEEPS", "BenchRow", "bench_sweep", "device_bytes", "format_table", "parse_sweep", "time_call",
 ]
