@@ -83,17 +83,94 @@ def _device_array(a: np.ndarray, dev):
     return torch.from_numpy(src).to(dev), shared
 
 
-def build_normal_equations(model: StateSpaceModel, *, device_out: bool = False):
+#: largest state / dense-measurement dimension of the hand-written assembly kernel (btd_kalman.cuh)
+KERNEL_MAX_DIM = 64
+
+
+def _raise_first_failure(info_q, info_r):
+    """NotPositiveDefinite for the first failing time step in the reference's loop order (process
+    covariance before measurement covariance at the same step, kalman.py:143-153); info_* are
+    1-based first failing pivots per step (0: fine)."""
+    import torch
+    bad = (info_q > 0) | (info_r > 0)
+    if not bool(bad.any()):
+        return
+    k = int(torch.nonzero(bad).flatten()[0])
+    if int(info_q[k]) > 0:
+        raise NotPositiveDefinite(int(info_q[k]), block=k, context="process covariance")
+    raise NotPositiveDefinite(int(info_r[k]), block=k, context="measurement covariance")
+
+
+def _build_batched(model: StateSpaceModel, dev):
+    """Large shapes (n or dense m > KERNEL_MAX_DIM, e.g. the paper's n = 256, m = 1024 case,
+    PAPER.md:632-641): the same algebra as the reference's per-step loop (kalman.py:99-162) as
+    batched GPU factorizations and products over the horizon (torch.linalg: cuSOLVER / cuBLAS --
+    harness code in front of the factor/solve path, not part of it).  Time-invariant H / Q / R
+    (stride-0 broadcasts) are factored once.  Returns (diag, sub, rhs) on the device."""
+    import torch
+    N, n, m = model.horizon, model.state_dim, model.obs_dim
+    G, _ = _device_array(model.transition, dev)
+    H, _ = _device_array(model.observation, dev)
+    Q, _ = _device_array(model.process_cov, dev)
+    R, _ = _device_array(model.measurement_cov, dev)
+    Z, _ = _device_array(model.observations, dev)
+    P, _ = _device_array(model.prior_offsets, dev)
+    # process covariance: Q^{-1}, Q^{-1} G_k, Q^{-1} zeta_k through its Cholesky factor
+    Lq, info_q = torch.linalg.cholesky_ex(Q)
+    if model.diagonal_measurement_cov:
+        bad = R <= 0.0
+        info_r = torch.where(bad.any(dim=1), bad.to(torch.int64).argmax(dim=1) + 1, 0)
+    else:
+        Lr, info_r = torch.linalg.cholesky_ex(R)
+    info_q = info_q.expand(N) if info_q.shape[0] == 1 else info_q
+    info_r = info_r.expand(N) if info_r.shape[0] == 1 else info_r
+    _raise_first_failure(info_q.cpu(), info_r.cpu())
+    eye = torch.eye(n, dtype=torch.float64, device=dev).expand(Lq.shape[0], n, n).contiguous()
+    q_inv = torch.cholesky_solve(eye, Lq)
+    q_inv_g = torch.cholesky_solve(G, Lq.expand(N, n, n) if Lq.shape[0] == 1 else Lq)
+    q_inv_zeta = torch.cholesky_solve(P.unsqueeze(-1), Lq.expand(N, n, n) if Lq.shape[0] == 1 else Lq)
+    # observation terms H^T R^{-1} H and H^T R^{-1} z (kalman.py:107-127)
+    if model.diagonal_measurement_cov:
+        weighted = H / R.unsqueeze(-1)
+        ht_ri_h = H.transpose(1, 2) @ weighted
+        ht_ri_z = H.transpose(1, 2) @ (Z / R).unsqueeze(-1)
+    else:
+        white_h = torch.linalg.solve_triangular(Lr, H, upper=False)
+        Lr_n = Lr.expand(N, m, m) if Lr.shape[0] == 1 else Lr
+        white_z = torch.linalg.solve_triangular(Lr_n, Z.unsqueeze(-1), upper=False)
+        ht_ri_h = white_h.transpose(1, 2) @ white_h
+        wh_n = white_h.expand(N, m, n) if white_h.shape[0] == 1 else white_h
+        ht_ri_z = wh_n.transpose(1, 2) @ white_z
+    diag = (q_inv + ht_ri_h).expand(N, n, n).clone()
+    rhs = ht_ri_z.expand(N, n, 1) + G.transpose(1, 2) @ q_inv_zeta
+    if N > 1:
+        diag[:-1] += G[1:].transpose(1, 2) @ q_inv_g[1:]
+    sub = -q_inv_g[1:].contiguous()
+    return diag.contiguous(), sub, rhs.contiguous()
+
+
+def build_normal_equations(model: StateSpaceModel, *, device_out: bool = False, _path: str = "auto"):
     """Smoothing normal equations (kalman.py:130-162), assembled on the GPU.
 
     Returns (BlockTridiagonalMatrix, BlockRhs) with numpy arenas (the reference's types), or torch
     CUDA tensors with ``device_out=True`` (ready for ``recursive_factorize`` without a round trip).
     Raises NotPositiveDefinite(pivot, block=k, context="process covariance" / "measurement
-    covariance") for the first failing time step, like the reference.
+    covariance") for the first failing time step, like the reference.  Shapes up to
+    KERNEL_MAX_DIM run in the hand-written assembly kernel; larger ones in batched library
+    factorizations (``_path`` = "kernel" / "batched" forces one, for tests).
     """
     import torch
     dev = torch.device("cuda", torch.cuda.current_device())
     N, n, m = model.horizon, model.state_dim, model.obs_dim
+    batched = _path == "batched" or (_path == "auto" and (
+        n > KERNEL_MAX_DIM or (m > KERNEL_MAX_DIM and not model.diagonal_measurement_cov)))
+    if batched:
+        from .core import new_btd
+        diag, sub, rhs = _build_batched(model, dev)
+        A = new_btd(N, n, diag, sub)  # the reference's symmetry check + (D + D^T)/2
+        if device_out:
+            return A, BlockRhs(rhs)
+        return BlockTridiagonalMatrix(A.diag.cpu().numpy(), A.sub.cpu().numpy()), BlockRhs(rhs.cpu().numpy())
     G, _ = _device_array(model.transition, dev)
     H, sh = _device_array(model.observation, dev)
     Q, sq = _device_array(model.process_cov, dev)

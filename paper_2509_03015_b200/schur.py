@@ -175,6 +175,27 @@ def _host_matrix(matrix: BlockTridiagonalMatrix):
     return d.ctypes.data, s.ctypes.data, (d, s)
 
 
+def _padded_size(n: int) -> int:
+    """Block size the kernels run at: n itself for n <= 64 (the level kernels pad in shared memory)
+    and for multiples of 64 (tiled path); otherwise the next multiple of 64.  A block padded with
+    an identity diagonal and zero couplings factors into the embedded original factor exactly (the
+    extra terms are exact zeros), so results and NPD coordinates are those of the n x n system."""
+    return n if n <= 64 or n % 64 == 0 else (n + 63) // 64 * 64
+
+
+def _pad_matrix(diag, sub, n: int, npad: int):
+    """Device arenas of size npad: identity on the padded diagonal, zero padded couplings."""
+    import torch
+    N = diag.shape[0]
+    dp = torch.zeros((N, npad, npad), dtype=torch.float64, device=diag.device)
+    dp[:, :n, :n] = diag
+    idx = torch.arange(n, npad, device=diag.device)
+    dp[:, idx, idx] = 1.0
+    sp = torch.zeros((sub.shape[0], npad, npad), dtype=torch.float64, device=diag.device)
+    sp[:, :n, :n] = sub
+    return dp, sp
+
+
 def recursive_factorize(matrix: BlockTridiagonalMatrix, config: RecursionConfig | None = None,
                         *, stream=None, profile: bool = False) -> FactorHierarchy:
     """Factor an SPD block-tridiagonal system for repeated solves (schur.py:289-318).
@@ -185,16 +206,19 @@ def recursive_factorize(matrix: BlockTridiagonalMatrix, config: RecursionConfig 
     import torch
     cfg = config or RecursionConfig()
     L = _native.lib()
-    N, n = matrix.num_blocks, matrix.block_size
+    N, n_user = matrix.num_blocks, matrix.block_size
+    n = _padded_size(n_user)
     st = _native.BtdStatus()
     handle = ctypes.c_void_p()
     c = cfg._c()
     rc = L.btd_create(N, n, ctypes.byref(c), ctypes.byref(handle), ctypes.byref(st))
     if rc != _native.BTD_OK:
         _raise_status(st, rc)
-    host = _host_matrix(matrix)
+    host = _host_matrix(matrix) if n == n_user else None
     if host is None:
         diag, sub = _device_matrix(matrix)
+        if n != n_user:
+            diag, sub = _pad_matrix(diag, sub, n_user, n)
     else:  # host-resident input: the C ABI overlaps the H2D copy with the level-0 elimination
         diag = torch.empty((N, n, n), dtype=torch.float64, device="cuda")
         sub = torch.empty((max(N - 1, 0), n, n), dtype=torch.float64, device="cuda")
@@ -204,6 +228,7 @@ def recursive_factorize(matrix: BlockTridiagonalMatrix, config: RecursionConfig 
     persistent = torch.empty(pers_b.value, dtype=torch.uint8, device=dev)
     scratch = torch.empty(scr_b.value, dtype=torch.uint8, device=dev)
     native = NativeFactor(handle, persistent, dev)
+    native.padded = n  # kernel block size (> n_user when padded)
     if profile:
         L.btd_profile_kernels(handle, 1)
     s = stream if stream is not None else torch.cuda.current_stream(dev)
@@ -225,7 +250,7 @@ def recursive_factorize(matrix: BlockTridiagonalMatrix, config: RecursionConfig 
         lnb, lp = ctypes.c_int64(), ctypes.c_int64()
         L.btd_level_info(handle, lvl, ctypes.byref(lnb), ctypes.byref(lp), None)
         levels.append(FactorLevel(lnb.value, lp.value, lvl, native))
-    return FactorHierarchy(N, n, levels, BaseFactor(nb.value, n), native)
+    return FactorHierarchy(N, n_user, levels, BaseFactor(nb.value, n_user), native)
 
 
 def recursive_solve(hierarchy: FactorHierarchy, rhs: BlockRhs, *, stream=None) -> BlockRhs:
@@ -253,6 +278,12 @@ def recursive_solve(hierarchy: FactorHierarchy, rhs: BlockRhs, *, stream=None) -
             b = b.to(native.device, non_blocking=True)
         b = b.to(torch.float64).contiguous()
     d = int(b.shape[2])
+    npad = getattr(native, "padded", hierarchy.block_size)
+    nu = hierarchy.block_size
+    if npad != nu:  # zero rows for the padded unknowns; the solution is the leading n rows
+        bp = torch.zeros((b.shape[0], npad, d), dtype=torch.float64, device=b.device)
+        bp[:, :nu] = b
+        b = bp
     x = torch.empty_like(b)
     scr_b = ctypes.c_size_t()
     L.btd_solve_workspace(native.handle, d, ctypes.byref(scr_b))
@@ -263,6 +294,8 @@ def recursive_solve(hierarchy: FactorHierarchy, rhs: BlockRhs, *, stream=None) -
                      ctypes.c_void_p(s.cuda_stream), ctypes.byref(st))
     if rc != _native.BTD_OK:
         _raise_status(st, rc)
+    if npad != nu:
+        x = x[:, :nu].contiguous()
     if host or host_tensor:
         # D2H into pinned memory (torch's caching host allocator): a pageable destination runs at a
         # fraction of the link bandwidth
@@ -307,7 +340,8 @@ def level_factor(hierarchy: FactorHierarchy, level: int):
     import torch
     native = hierarchy._native
     L = _native.lib()
-    n = hierarchy.block_size
+    nu = hierarchy.block_size
+    n = getattr(native, "padded", nu)
     N = hierarchy.base.num_blocks if level == len(hierarchy.levels) else hierarchy.levels[level].num_blocks
     linv = torch.empty((N, n, n), dtype=torch.float64, device=native.device)
     lsub = torch.empty((max(N - 1, 0), n, n), dtype=torch.float64, device=native.device)
@@ -316,4 +350,4 @@ def level_factor(hierarchy: FactorHierarchy, level: int):
                             ctypes.c_void_p(torch.cuda.current_stream(native.device).cuda_stream), ctypes.byref(st))
     if rc != _native.BTD_OK:
         _raise_status(st, rc)
-    return linv, lsub
+    return linv[:, :nu, :nu], lsub[:, :nu, :nu]

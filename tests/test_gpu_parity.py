@@ -73,6 +73,8 @@ SWEEP = [  # (N, n, d, crossover, rho)
     (200, 31, 2, 16, 5), (300, 33, 1, 64, 8), (111, 47, 4, 9, 4), (250, 63, 1, 64, 8),
     (260, 64, 3, 64, 8), (1000, 8, 1, 64, 8), (777, 12, 5, 10, 7), (90, 64, 6, 4, 2), (45, 6, 9, 3, 16),
     (20, 128, 2, 4, 3), (70, 256, 3, 8, 8), (9, 192, 1, 2, 2), (3, 128, 65, 1, 1), (50, 256, 70, 64, 8),
+    # n > 64 and not a multiple of 64: padded to the next multiple of 64 (schur._padded_size)
+    (90, 80, 2, 8, 4), (40, 100, 1, 64, 8), (25, 65, 3, 4, 2), (12, 150, 2, 2, 2),
 ]
 
 
@@ -208,3 +210,24 @@ def test_npd_coordinates_every_kernel_vs_oracle(N, n, rho, cross, bad):
                                 pkg.RecursionConfig(crossover=cross, segment_length=rho))
     o, g = eo.value, eg.value
     assert (g.pivot, g.level, g.member, g.block) == (o.pivot, o.level, o.member, o.block)
+
+
+def test_padded_block_size_npd_coordinates_and_introspection():
+    """n = 100 runs padded to 128: a non-positive pivot reports the n x n system's coordinates, and
+    level_factor returns n x n blocks (the embedded factor)."""
+    N, n = 300, 100
+    A, B = pkg.generate_spd_btd(N, n, 1, seed=4)
+    diag = A.diag.copy()
+    diag[123, 37, 37] = -80.0
+    with pytest.raises(pkg.NotPositiveDefinite) as e:
+        pkg.recursive_factorize(pkg.BlockTridiagonalMatrix(diag, A.sub))
+    with pytest.raises(port.OracleNPD) as eo:
+        port.factorize(diag, A.sub)
+    want = (eo.value.pivot, eo.value.level, eo.value.member, eo.value.block)
+    assert (e.value.pivot, e.value.level, e.value.member, e.value.block) == want
+    h = pkg.recursive_factorize(A)
+    linv, lsub = pkg.level_factor(h, 0)
+    assert tuple(linv.shape) == (N, n, n) and tuple(lsub.shape) == (N - 1, n, n)
+    X = pkg.recursive_solve(h, B)
+    assert X.blocks.shape == (N, n, 1)
+    assert pkg.residual_report(A, X, B)[1] <= REL_RES
