@@ -115,6 +115,28 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
                : "memory");
 }
 
+// The same with an L2 eviction-priority hint (createpolicy): evict_last for data that is read
+// again soon (a solve's forward-sweep blocks, re-read by the backward sweep), evict_first for the
+// last use.
+__device__ __forceinline__ unsigned long long l2_policy_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long l2_policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                                 unsigned long long policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
 // Bulk prefetch of a contiguous global range into L2 (cp.async.bulk.prefetch.L2, no completion
 // tracking): used to pull the next step's diagonal block into L2 while the Cholesky runs.
 __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {

@@ -290,16 +290,20 @@ struct TmaShape {
   static constexpr int NCW = S::NTHREADS / 32;  // consumer warps
   static constexpr int NTHREADS = S::NTHREADS + 32;
 #ifndef BTD_TMA_STAGES64
-#define BTD_TMA_STAGES64 4
+#define BTD_TMA_STAGES64 2  // n = 64, d = 1: two CTAs per SM (two segments in flight), 2-slot rings
 #endif
   static constexpr int STAGES = NT == 64 ? (DC > 1 ? 3 : BTD_TMA_STAGES64) : 8;
   static constexpr int STAGE = S::FULL + S::PACK + NT * DC;  // doubles per slot
+#ifndef BTD_SOLVE_MINB
+#define BTD_SOLVE_MINB 2
+#endif
+  static constexpr int MINB = (NT == 64 && DC == 1) ? BTD_SOLVE_MINB : 1;  // resident CTAs per SM
   static constexpr size_t SMEM = sizeof(double) * ((size_t)STAGES * STAGE + (size_t)(4 + S::ZMAX) * NT * DC) +
                                  2 * STAGES * sizeof(unsigned long long);
 };
 
 template <int NT, int DC>
-__global__ void __launch_bounds__(TmaShape<NT, DC>::NTHREADS) solve_tma_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(TmaShape<NT, DC>::NTHREADS, TmaShape<NT, DC>::MINB) solve_tma_kernel(SolveArgs a) {
   using S = Solve2Shape<NT>;
   using T = TmaShape<NT, DC>;
   constexpr int STAGES = T::STAGES, STAGE = T::STAGE, NTH = S::NTHREADS;
@@ -334,6 +338,9 @@ __global__ void __launch_bounds__(TmaShape<NT, DC>::NTHREADS) solve_tma_kernel(S
     if (lane == 0) {
       int slot = 0;
       unsigned phase = 0;
+#ifndef BTD_SOLVE_NOHINT
+      const unsigned long long pol_keep = l2_policy_evict_last(), pol_drop = l2_policy_evict_first();
+#endif
       constexpr unsigned fb = NT * NT * sizeof(double), pb = S::PACK * sizeof(double);
       const unsigned vb = (unsigned)(n * d * sizeof(double));
       SegBounds sb(a, mode, blockIdx.x, K);
@@ -368,8 +375,16 @@ __global__ void __launch_bounds__(TmaShape<NT, DC>::NTHREADS) solve_tma_kernel(S
           full = pack = vec = nullptr;
 #endif
           mbar_arrive_expect_tx(&full_bar[slot], (full ? fb : 0) + (pack ? pb : 0) + (vec ? vb : 0));
+#ifndef BTD_SOLVE_NOHINT
+          // forward-sweep blocks are read again by the backward sweep: keep them in L2 (evict_last);
+          // the backward sweep is their last use (evict_first)
+          const unsigned long long pol = (kind == kStepF) ? pol_keep : pol_drop;
+          if (full) tma_load_1d_hint(st, full, fb, &full_bar[slot], pol);
+          if (pack) tma_load_1d_hint(st + S::FULL, pack, pb, &full_bar[slot], pol);
+#else
           if (full) tma_load_1d(st, full, fb, &full_bar[slot]);
           if (pack) tma_load_1d(st + S::FULL, pack, pb, &full_bar[slot]);
+#endif
           if (vec) tma_load_1d(st + S::FULL + S::PACK, vec, vb, &full_bar[slot]);
           if (++slot == STAGES) {
             slot = 0;
