@@ -137,6 +137,13 @@ __device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, uns
       : "memory");
 }
 
+// Scalar global load with an L2 eviction-priority policy (see l2_policy_*).
+__device__ __forceinline__ double ld_hint(const double* p, unsigned long long policy) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(policy));
+  return v;
+}
+
 // Bulk prefetch of a contiguous global range into L2 (cp.async.bulk.prefetch.L2, no completion
 // tracking): used to pull the next step's diagonal block into L2 while the Cholesky runs.
 __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {

@@ -45,7 +45,10 @@ __device__ __forceinline__ void store_row8(double* blk, const double (&v)[8], in
     if (c < n) blk[r * n + c] = v[c];
 }
 
-__global__ void __launch_bounds__(kSmallThreads, 3) factor_small_kernel(FactorArgs a) {
+#ifndef BTD_FSMALL_MINB
+#define BTD_FSMALL_MINB 3
+#endif
+__global__ void __launch_bounds__(kSmallThreads, BTD_FSMALL_MINB) factor_small_kernel(FactorArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 3, r = lane & 7;
   const bool coupled = !a.base;
@@ -228,15 +231,21 @@ __global__ void __launch_bounds__(kSmallThreads) solve_small_kernel(SolveArgs a)
   };
   // operand rows of one step, loaded a step ahead of their use (the sweeps are memory-latency
   // bound: 8-lane groups, a few hundred cycles of shuffles per step against ~1 us of DRAM latency)
+  // L2 priority: the forward sweep's blocks are re-read by the backward sweep (evict_last), which
+  // is their last use (evict_first); thousands of segments are in flight per level
+  const unsigned long long pol_keep = l2_policy_evict_last(), pol_drop = l2_policy_evict_first();
   auto ld_full = [&](const double* M, bool trans, double (&m8)[8], bool ok) {  // row r of M or M^T
+    const unsigned long long pol = trans ? pol_drop : pol_keep;  // trans <=> backward sweep / fold
 #pragma unroll
-    for (int q = 0; q < 8; ++q) m8[q] = (ok && rv && q < n) ? (trans ? M[(size_t)q * n + r] : M[(size_t)r * n + q]) : 0.0;
+    for (int q = 0; q < 8; ++q)
+      m8[q] = (ok && rv && q < n) ? ld_hint(trans ? M + (size_t)q * n + r : M + (size_t)r * n + q, pol) : 0.0;
   };
   auto ld_pack = [&](const double* P, bool trans, double (&m8)[8], bool ok) {  // row r of Linv or Linv^T
+    const unsigned long long pol = trans ? pol_drop : pol_keep;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const bool in = ok && rv && q < n && (trans ? q >= r : q <= r);
-      m8[q] = in ? (trans ? P[packed_offset_(q) + r] : P[packed_offset_(r) + q]) : 0.0;
+      m8[q] = in ? ld_hint(trans ? P + packed_offset_(q) + r : P + packed_offset_(r) + q, pol) : 0.0;
     }
   };
   // y (+)= sign * m8 . v  (v broadcast inside the group)
