@@ -264,27 +264,43 @@ cudaError_t dispatch_solve_dc(const btd::SolveArgs& a, unsigned grid_x, cudaStre
   return launch_solve<NT, 4>(a, grid_x, s);
 }
 
-template <int NT, int DC>
-cudaError_t launch_stream(const btd::SolveArgs& a, cudaStream_t s) {
-  using T = btd::TmaShape<NT, DC>;
+template <int NT, int DC, bool WIDE>
+cudaError_t launch_stream_v(const btd::SolveArgs& a, cudaStream_t s) {
+  using T = btd::TmaShape<NT, DC, WIDE>;
   static int blocks_per_sm = -1, sms = 0;
   if (blocks_per_sm < 0) {
-    cudaError_t e = cudaFuncSetAttribute(btd::solve_tma_kernel<NT, DC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)T::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(btd::solve_tma_kernel<NT, DC, WIDE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM);
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, btd::solve_tma_kernel<NT, DC>, T::NTHREADS,
-                                                      T::SMEM);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, btd::solve_tma_kernel<NT, DC, WIDE>,
+                                                      T::NTHREADS, T::SMEM);
     if (e != cudaSuccess) return e;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   const long long cap = (long long)blocks_per_sm * sms;
   const unsigned gx = (unsigned)(a.K < cap ? a.K : cap);
   dim3 grid(gx, (unsigned)((a.d + DC - 1) / DC));
-  btd::solve_tma_kernel<NT, DC><<<grid, T::NTHREADS, T::SMEM, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
+  btd::solve_tma_kernel<NT, DC, WIDE><<<grid, T::NTHREADS, T::SMEM, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
+}
+
+// Wide levels (at least as many segments as SMs) at n = 64, d = 1 run two CTAs per SM; narrow
+// levels and the base keep one CTA per SM with a 4-slot ring (deeper prefetch for the lone segment).
+template <int NT, int DC>
+cudaError_t launch_stream(const btd::SolveArgs& a, cudaStream_t s) {
+  if constexpr (NT == 64 && DC == 1) {
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    if (a.mode != btd::kSolveBase && a.K >= sms) return launch_stream_v<NT, DC, true>(a, s);
+  }
+  return launch_stream_v<NT, DC, false>(a, s);
 }
 
 template <int NT>

@@ -284,28 +284,26 @@ struct SegBounds {
   }
 };
 
-template <int NT, int DC>
+// WIDE (levels with at least as many segments as SMs, n = 64, d = 1): two CTAs per SM (two
+// segments in flight per SM) with 2-slot rings; otherwise one CTA per SM with a deeper ring.
+template <int NT, int DC, bool WIDE = false>
 struct TmaShape {
   using S = Solve2Shape<NT>;
   static constexpr int NCW = S::NTHREADS / 32;  // consumer warps
   static constexpr int NTHREADS = S::NTHREADS + 32;
-#ifndef BTD_TMA_STAGES64
-#define BTD_TMA_STAGES64 2  // n = 64, d = 1: two CTAs per SM (two segments in flight), 2-slot rings
-#endif
-  static constexpr int STAGES = NT == 64 ? (DC > 1 ? 3 : BTD_TMA_STAGES64) : 8;
+  static constexpr bool TWO = WIDE && NT == 64 && DC == 1;
+  static constexpr int STAGES = NT == 64 ? (DC > 1 ? 3 : (TWO ? 2 : 4)) : 8;
   static constexpr int STAGE = S::FULL + S::PACK + NT * DC;  // doubles per slot
-#ifndef BTD_SOLVE_MINB
-#define BTD_SOLVE_MINB 2
-#endif
-  static constexpr int MINB = (NT == 64 && DC == 1) ? BTD_SOLVE_MINB : 1;  // resident CTAs per SM
+  static constexpr int MINB = TWO ? 2 : 1;  // resident CTAs per SM (register cap 112 when 2)
   static constexpr size_t SMEM = sizeof(double) * ((size_t)STAGES * STAGE + (size_t)(4 + S::ZMAX) * NT * DC) +
                                  2 * STAGES * sizeof(unsigned long long);
 };
 
-template <int NT, int DC>
-__global__ void __launch_bounds__(TmaShape<NT, DC>::NTHREADS, TmaShape<NT, DC>::MINB) solve_tma_kernel(SolveArgs a) {
+template <int NT, int DC, bool WIDE>
+__global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT, DC, WIDE>::MINB)
+    solve_tma_kernel(SolveArgs a) {
   using S = Solve2Shape<NT>;
-  using T = TmaShape<NT, DC>;
+  using T = TmaShape<NT, DC, WIDE>;
   constexpr int STAGES = T::STAGES, STAGE = T::STAGE, NTH = S::NTHREADS;
   extern __shared__ __align__(16) double smem[];
   double* ring = smem;
