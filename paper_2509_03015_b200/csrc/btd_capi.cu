@@ -402,11 +402,37 @@ struct BigCtx {
   cudaStream_t s;
   int k0 = 0;
   int Kws = 0;  // segments the per-segment workspaces are laid out for (0: K)
+  // segment lengths present in this launch sequence (regular plan: all segments but the last
+  // have the same length); 0 = unknown (every launch is issued)
+  int jreg = 0, jtail = 0;
 };
+
+void set_lengths(BigCtx& c, const LevelPlan& lp) {
+  if (lp.K < 1) return;
+  c.jreg = (int)(lp.sep(1) - lp.sep(0) - 1);
+  c.jtail = (int)(lp.sep(lp.K) - lp.sep(lp.K - 1) - 1);
+}
+
+// Does any segment of the sequence do work at step j for this activity?  Launches that would only
+// start CTAs to exit (e.g. the last-row products at every other step) are skipped on the host.
+bool big_any_active(const BigCtx& c, int j, int act) {
+  if (!c.jreg) return true;
+  auto hit = [&](int J) {
+    switch (act) {
+      case btd::kActNotLast: return j < J - 1;
+      case btd::kActLast: return j == J - 1;
+      case btd::kActBeforeSecondLast: return j < J - 2;
+      case btd::kActSecondLast: return j == J - 2;
+      default: return j < J;
+    }
+  };
+  return hit(c.jreg) || hit(c.jtail);
+}
 
 cudaError_t big_gemm(const BigCtx& c, int j, int act, btd::Operand A, btd::Operand B, btd::Operand Cin,
                      btd::Operand Cout, int m, int n, int k, double alpha, double beta, int lower = 0, int tri = 0,
                      int store_trans = 0) {
+  if (!big_any_active(c, j, act)) return cudaSuccess;
   static bool configured = false;
   const int smem = 4 * btd::GSTAGE * (int)sizeof(double);  // 2 stages x (A, B) tiles
   if (!configured) {
@@ -449,6 +475,7 @@ cudaError_t big_gemm(const BigCtx& c, int j, int act, btd::Operand A, btd::Opera
 }
 
 cudaError_t big_copy(const BigCtx& c, int j, int act, btd::Operand src, btd::Operand dst, int rows, int cols) {
+  if (!big_any_active(c, j, act)) return cudaSuccess;
   btd::CopyArgs a{};
   a.src = src;
   a.dst = dst;
@@ -1112,6 +1139,7 @@ static int enqueue_factor(btd_hierarchy* h, const double* diag, const double* su
       int jmax = 0;
       jmax = (int)lp.max_segment();
       BigCtx c{(const int*)(pers + lp.off_seps), lp.N, 0, (int)lp.K, err, stream};
+      set_lengths(c, lp);
       double* next_diag = (double*)(scr + lp.off_next_diag);
       prof_mark(h, stream);
       auto level_seq = [&](const BigCtx& cc) {
@@ -1154,6 +1182,7 @@ static int enqueue_factor(btd_hierarchy* h, const double* diag, const double* su
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize_partial(export)");
     } else if (!h->overflow) {
       BigCtx c{nullptr, h->base_N, 1, 1, err, stream};
+      c.jreg = c.jtail = (int)h->base_N;
       prof_mark(h, stream);
       e = big_factor_level(c, (int)h->levels.size(), (int)h->base_N, n, cd, cs, (double*)(pers + h->off_base_linv),
                            (double*)(pers + h->off_base_lsub), nullptr, nullptr, nullptr, scr + h->off_big_ws, err);
@@ -1349,6 +1378,7 @@ static int enqueue_solve(const btd_hierarchy* h, const double* rhs, double* x, i
       jmax = (int)lp.max_segment();
       const int* sp = (const int*)(pers + lp.off_seps);
       BigCtx c{sp, lp.N, 0, (int)lp.K, err, stream};
+      set_lengths(c, lp);
       e = big_solve_level(c, btd::kSolveDown, jmax, n, dd, rhs_l[l], (const double*)(pers + lp.off_linv),
                           (const double*)(pers + lp.off_lsub), x_l[l], nullptr, rhs_l[l + 1], fr_l[l], Tws, Uws);
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(big down)");
@@ -1366,6 +1396,7 @@ static int enqueue_solve(const btd_hierarchy* h, const double* rhs, double* x, i
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve_up(import)");
     } else {
       BigCtx c{nullptr, h->base_N, 1, 1, err, stream};
+      c.jreg = c.jtail = (int)h->base_N;
       e = big_solve_level(c, btd::kSolveBase, (int)h->base_N, n, dd, rhs_l[L], (const double*)(pers + h->off_base_linv),
                           (const double*)(pers + h->off_base_lsub), x_l[L], nullptr, nullptr, nullptr, Tws, Uws);
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(big base)");
@@ -1376,6 +1407,7 @@ static int enqueue_solve(const btd_hierarchy* h, const double* rhs, double* x, i
       jmax = (int)lp.max_segment();
       const int* sp = (const int*)(pers + lp.off_seps);
       BigCtx c{sp, lp.N, 0, (int)lp.K, err, stream};
+      set_lengths(c, lp);
       const long long nn = (long long)n * n, ps = (long long)n * dd;
       const double* Ls = (const double*)(pers + lp.off_lsub);
       // boundary-modified rhs: b_0 -= C_L x_L ; b_last -= C_R^T x_R
