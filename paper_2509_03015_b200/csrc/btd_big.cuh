@@ -75,6 +75,8 @@ struct GemmArgs {
   int store_trans;       // write Cout^T
   int tiles_n;
   int k0;                // first segment of this launch (blockIdx.y = k - k0)
+  int ksplit;            // > 1: split-k over ksplit CTAs per tile, raw partials into `part`
+  double* part;          //      (tile, split, 64 x 64), summed in split order by bt_gemm_reduce_kernel
   const DevErr* err;
 };
 
@@ -177,7 +179,9 @@ __global__ void __launch_bounds__(BTHREADS) bt_gemm_kernel(GemmArgs g) {
   const int k = g.k0 + blockIdx.y;
   int J;
   if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, g.act, J)) return;
-  const int tm = blockIdx.x / g.tiles_n, tn = blockIdx.x % g.tiles_n;
+  const int ks = g.ksplit > 1 ? g.ksplit : 1;
+  const int tile = blockIdx.x / ks, sp = blockIdx.x % ks;
+  const int tm = tile / g.tiles_n, tn = tile % g.tiles_n;
   const int m0 = tm * BT, n0 = tn * BT;
   if (g.lower_only && n0 > m0) return;
   extern __shared__ __align__(16) double gsm[];
@@ -187,8 +191,26 @@ __global__ void __launch_bounds__(BTHREADS) bt_gemm_kernel(GemmArgs g) {
   if (g.tri == 1) kend = min(kend, n0 + BT);
   if (g.tri == 2) kend = min(kend, m0 + BT);
   if (g.tri == 3) kbeg = m0 / BT * BT;
+  if (ks > 1) {  // this CTA's share of the k range, in whole BK chunks
+    const int chunk = ((kend - kbeg + ks - 1) / ks + BK - 1) / BK * BK;
+    const int b = kbeg + sp * chunk;
+    kend = min(kend, b + chunk);
+    kbeg = b;
+  }
   double acc[2][4][2];
   gemm_tile_pipelined<TA, TB>(acc, A, g.A.ld, B, g.B.ld, g.m, g.n, g.k, m0, n0, kbeg, kend, gsm);
+  if (ks > 1) {  // raw partial of (tile, sp)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int rw = (warp >> 1) * 16, cw = (warp & 1) * 32;
+    double* pt = g.part + ((size_t)tile * ks + sp) * BT * BT;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<double2*>(pt + (rw + i * 8 + (lane >> 2)) * BT + cw + q * 8 + 2 * (lane & 3)) =
+            make_double2(acc[i][q][0], acc[i][q][1]);
+    return;
+  }
   const double* Cin = g.beta != 0.0 ? operand_ptr(g.Cin, g.seps, g.base_mode, k, g.j) : nullptr;
   if (Cin) Cin += (size_t)g.Cin.row0 * g.Cin.ld + g.Cin.col0;
   double* Cout = const_cast<double*>(operand_ptr(g.Cout, g.seps, g.base_mode, k, g.j)) +
@@ -211,6 +233,35 @@ __global__ void __launch_bounds__(BTHREADS) bt_gemm_kernel(GemmArgs g) {
         else
           Cout[(size_t)r * g.Cout.ld + c] = v;
       }
+}
+
+// Split-k epilogue: C = alpha * (sum of the partials in split order) + beta * Cin, per 64 x 64 tile
+// (deterministic: fixed summation order).  grid.x = tiles, blockIdx.y = segment (as the GEMM).
+__global__ void __launch_bounds__(BTHREADS) bt_gemm_reduce_kernel(GemmArgs g) {
+  if (error_raised(g.err)) return;
+  const int k = g.k0 + blockIdx.y;
+  int J;
+  if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, g.act, J)) return;
+  const int tile = blockIdx.x, tm = tile / g.tiles_n, tn = tile % g.tiles_n;
+  const int m0 = tm * BT, n0 = tn * BT;
+  if (g.lower_only && n0 > m0) return;
+  const double* Cin = g.beta != 0.0 ? operand_ptr(g.Cin, g.seps, g.base_mode, k, g.j) : nullptr;
+  if (Cin) Cin += (size_t)g.Cin.row0 * g.Cin.ld + g.Cin.col0;
+  double* Cout = const_cast<double*>(operand_ptr(g.Cout, g.seps, g.base_mode, k, g.j)) +
+                 (size_t)g.Cout.row0 * g.Cout.ld + g.Cout.col0;
+  const double* pt = g.part + (size_t)tile * g.ksplit * BT * BT;
+  for (int e = threadIdx.x; e < BT * BT; e += BTHREADS) {
+    const int r = m0 + e / BT, c = n0 + e % BT;
+    if (r >= g.m || c >= g.n) continue;
+    double s = 0.0;
+    for (int q = 0; q < g.ksplit; ++q) s += pt[(size_t)q * BT * BT + e];
+    double v = g.alpha * s;
+    if (Cin) v += g.beta * Cin[(size_t)r * g.Cin.ld + c];
+    if (g.store_trans)
+      Cout[(size_t)c * g.Cout.ld + r] = v;
+    else
+      Cout[(size_t)r * g.Cout.ld + c] = v;
+  }
 }
 
 struct CopyArgs {

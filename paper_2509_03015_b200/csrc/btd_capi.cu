@@ -63,6 +63,7 @@ struct btd_hierarchy {
   bool partial = false;          // sharded chunk: exactly `levels` local levels, no base
   int64_t kmax = 1;              // most segments of any level (big-path workspaces)
   size_t off_big_ws = 0;         // factor scratch: WD | WX | WP per segment
+  size_t off_splitk = 0;         // factor scratch: split-k partials of the base GEMMs
   size_t persistent_bytes = 0, scratch_bytes = 0;
   char* persistent = nullptr;
   bool factored = false;
@@ -405,7 +406,14 @@ struct BigCtx {
   // segment lengths present in this launch sequence (regular plan: all segments but the last
   // have the same length); 0 = unknown (every launch is issued)
   int jreg = 0, jtail = 0;
+  double* part = nullptr;  // split-k partials workspace (single-segment sequences: the serial base)
+  size_t part_doubles = 0;
 };
+
+// split-k partials of the base solve's n x d products: 8 splits of ceil(n/64) x ceil(d/64) tiles
+size_t big_solve_part_doubles(int64_t n, int64_t d) {
+  return (size_t)8 * ((n + 63) / 64) * ((d + 63) / 64) * 64 * 64;
+}
 
 void set_lengths(BigCtx& c, const LevelPlan& lp) {
   if (lp.K < 1) return;
@@ -465,12 +473,33 @@ cudaError_t big_gemm(const BigCtx& c, int j, int act, btd::Operand A, btd::Opera
   g.tiles_n = (n + btd::BT - 1) / btd::BT;
   g.k0 = c.k0;
   g.err = c.err;
-  dim3 grid((unsigned)(((m + btd::BT - 1) / btd::BT) * g.tiles_n), (unsigned)c.K);
+  const int tiles = ((m + btd::BT - 1) / btd::BT) * g.tiles_n;
+  // split-k when the grid is far too small for the machine (the serial base: one segment) and k is
+  // long enough to pay for the extra reduce launch (measured: a loss at k = 128/256, a gain at 1024)
+  g.ksplit = 1;
+  if (c.part && c.K == 1 && k >= 512) {
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int ks = std::min(8, std::max(1, sms / std::max(1, 2 * tiles)));
+    ks = std::min(ks, std::max(1, k / btd::BK));
+    while (ks > 1 && (size_t)tiles * ks * btd::BT * btd::BT > c.part_doubles) --ks;
+    g.ksplit = ks;
+    g.part = c.part;
+  }
+  dim3 grid((unsigned)(tiles * g.ksplit), (unsigned)c.K);
   if (!A.trans && !B.trans) btd::bt_gemm_kernel<false, false><<<grid, btd::BTHREADS, smem, c.s>>>(g);
   else if (!A.trans) btd::bt_gemm_kernel<false, true><<<grid, btd::BTHREADS, smem, c.s>>>(g);
   else if (!B.trans) btd::bt_gemm_kernel<true, false><<<grid, btd::BTHREADS, smem, c.s>>>(g);
   else btd::bt_gemm_kernel<true, true><<<grid, btd::BTHREADS, smem, c.s>>>(g);
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (g.ksplit > 1) {
+    btd::bt_gemm_reduce_kernel<<<dim3((unsigned)tiles, (unsigned)c.K), btd::BTHREADS, 0, c.s>>>(g);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
   return cudaGetLastError();
 }
 
@@ -937,6 +966,8 @@ static int create_impl(int64_t num_blocks, int64_t block_size, const btd_config*
   if (big) {
     h->off_big_ws = so;
     so = align_up(so + (size_t)h->kmax * 5 * bb);
+    h->off_splitk = so;  // split-k partials of the base's n x n products (8 splits)
+    so = align_up(so + (size_t)8 * bb);
   }
   h->scratch_bytes = std::max<size_t>(so, kAlign);
   *out = h;
@@ -1183,6 +1214,8 @@ static int enqueue_factor(btd_hierarchy* h, const double* diag, const double* su
     } else if (!h->overflow) {
       BigCtx c{nullptr, h->base_N, 1, 1, err, stream};
       c.jreg = c.jtail = (int)h->base_N;
+      c.part = (double*)(scr + h->off_splitk);
+      c.part_doubles = (size_t)8 * h->n * h->n;
       prof_mark(h, stream);
       e = big_factor_level(c, (int)h->levels.size(), (int)h->base_N, n, cd, cs, (double*)(pers + h->off_base_linv),
                            (double*)(pers + h->off_base_lsub), nullptr, nullptr, nullptr, scr + h->off_big_ws, err);
@@ -1333,10 +1366,11 @@ int btd_solve_workspace(const btd_hierarchy* h, int64_t d, size_t* scratch_bytes
     so = align_up(so + (size_t)lp.P * pb);  // next x
     so = align_up(so + (size_t)lp.K * pb);  // f_R
   }
-  if (h->big) {  // T, U panels per segment and the boundary-modified rhs of a level
+  if (h->big) {  // T, U panels per segment, the boundary-modified rhs of a level, split-k partials
     so = align_up(so + (size_t)h->kmax * pb);
     so = align_up(so + (size_t)h->kmax * pb);
     so = align_up(so + (size_t)h->N * pb);
+    so = align_up(so + big_solve_part_doubles(h->n, d) * sizeof(double));
   }
   if (scratch_bytes) *scratch_bytes = std::max<size_t>(so, kAlign);
   return BTD_OK;
@@ -1371,6 +1405,8 @@ static int enqueue_solve(const btd_hierarchy* h, const double* rhs, double* x, i
     double* Uws = (double*)(scr + so);
     so = align_up(so + (size_t)h->kmax * pb);
     double* rmod = (double*)(scr + so);
+    so = align_up(so + (size_t)h->N * pb);
+    double* part = (double*)(scr + so);  // split-k partials (serial base)
     const int dd = (int)d;
     for (size_t l = 0; l < L && phase != kPhaseUp; ++l) {
       const LevelPlan& lp = h->levels[l];
@@ -1397,6 +1433,8 @@ static int enqueue_solve(const btd_hierarchy* h, const double* rhs, double* x, i
     } else {
       BigCtx c{nullptr, h->base_N, 1, 1, err, stream};
       c.jreg = c.jtail = (int)h->base_N;
+      c.part = part;
+      c.part_doubles = big_solve_part_doubles(h->n, d);
       e = big_solve_level(c, btd::kSolveBase, (int)h->base_N, n, dd, rhs_l[L], (const double*)(pers + h->off_base_linv),
                           (const double*)(pers + h->off_base_lsub), x_l[L], nullptr, nullptr, nullptr, Tws, Uws);
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(big base)");
