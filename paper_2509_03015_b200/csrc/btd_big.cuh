@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(BTHREADS) bt_gemm_kernel(GemmArgs g) {
   if (g.tri == 1) kend = min(kend, n0 + BT);
   if (g.tri == 2) kend = min(kend, m0 + BT);
   if (g.tri == 3) kbeg = m0 / BT * BT;
+  if (g.tri == 4) kbeg = max(kbeg, n0 / BT * BT);  // op(B)[k][c] == 0 for k < c (B lower triangular)
   if (ks > 1) {  // this CTA's share of the k range, in whole BK chunks
     const int chunk = ((kend - kbeg + ks - 1) / ks + BK - 1) / BK * BK;
     const int b = kbeg + sp * chunk;
@@ -262,6 +263,62 @@ __global__ void __launch_bounds__(BTHREADS) bt_gemm_reduce_kernel(GemmArgs g) {
     else
       Cout[(size_t)r * g.Cout.ld + c] = v;
   }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Host-sequenced blocked Cholesky + inverse of the n x n blocks (big_potrf_seq, btd_capi.cu): the
+// 64 x 64 diagonal tiles are factored and inverted here (one 128-thread CTA per segment,
+// potrf_trtri<64>), the panel / trailing / inverse products run as batched tile GEMMs over every
+// segment and tile -- the machine-wide parallelism the one-CTA-per-block kernel lacks.
+// ---------------------------------------------------------------------------------------------
+struct BigDiagArgs {
+  Operand D, Linv;  // segment's working block (in: updated D; tile kb factored) and Linv output
+  const int* seps;
+  long long N;
+  int base_mode, j, kb, n, level, k0;
+  DevErr* err;
+};
+
+__global__ void __launch_bounds__(128) big_diag_potrf_kernel(BigDiagArgs g) {
+  constexpr int LD = FactorShape<64>::LD;
+  if (error_raised(g.err)) return;
+  const int k = g.k0 + blockIdx.x;
+  int J;
+  if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, kActAll, J)) return;
+  __shared__ __align__(16) double DL[BT * LD];
+  __shared__ int s_fail;
+  const double* D = operand_ptr(g.D, g.seps, g.base_mode, k, g.j);
+  double* Li = const_cast<double*>(operand_ptr(g.Linv, g.seps, g.base_mode, k, g.j));
+  const int n = g.n, o = g.kb * BT;
+  for (int e = threadIdx.x; e < BT * BT; e += 128) DL[(e / BT) * LD + e % BT] = D[(size_t)(o + e / BT) * n + o + e % BT];
+  __syncthreads();
+  const int fail = potrf_trtri<64>(DL, &s_fail);  // warps 0..3 = group A
+  if (fail) {
+    if (threadIdx.x == 0) report_npd(g.err, g.level, g.j, k, o + fail);
+    return;
+  }
+  for (int e = threadIdx.x; e < BT * BT; e += 128) {
+    const int r = e / BT, c = e % BT;
+    Li[(size_t)(o + r) * n + o + c] = c <= r ? DL[r * LD + c] : 0.0;
+  }
+}
+
+// zero the strict upper 64 x 64 tiles of every active segment's n x n Linv (grid.x = tile pairs)
+__global__ void big_zero_upper_kernel(BigDiagArgs g) {
+  if (error_raised(g.err)) return;
+  const int k = g.k0 + blockIdx.y;
+  int J;
+  if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, kActAll, J)) return;
+  double* Li = const_cast<double*>(operand_ptr(g.Linv, g.seps, g.base_mode, k, g.j));
+  int t = blockIdx.x, ib = 0;
+  const int NB = g.n / BT;
+  while (t >= NB - 1 - ib) {  // pair t -> (ib, jb > ib)
+    t -= NB - 1 - ib;
+    ++ib;
+  }
+  const int jb = ib + 1 + t;
+  for (int e = threadIdx.x; e < BT * BT; e += blockDim.x)
+    Li[(size_t)(ib * BT + e / BT) * g.n + jb * BT + e % BT] = 0.0;
 }
 
 struct CopyArgs {

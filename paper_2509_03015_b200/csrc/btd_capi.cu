@@ -562,6 +562,86 @@ cudaError_t ensure_aux(btd_hierarchy* h) {
   return e;
 }
 
+// Blocked Cholesky + inverse of the n x n working blocks of one step (replaces big_potrf_kernel when
+// big_seq_potrf says so): per 64-column block kb the diagonal tile (big_diag_potrf_kernel), the
+// panel L_ib = A_ib Linv_kk^T and the trailing update A_ij -= L_ib L_jb^T as batched tile GEMMs;
+// then the inverse row by row, Linv[i][0:i] = -Linv_ii (L[i][0:i] Linv[0:i][0:i]) with the inner
+// product parked transposed in the unused strict upper tiles of the working block.
+cudaError_t big_potrf_seq(const BigCtx& c, int level, int j, int n, double* WD, double* Linv, btd::DevErr* err) {
+  using namespace btd;
+  const int NB = n / BT;
+  const long long nn = (long long)n * n;
+  auto D_at = [&](int r0, int c0, int trans = 0) {
+    Operand o = opnd(WD, nn, n, kIdxSeg);
+    o.row0 = r0;
+    o.col0 = c0;
+    o.trans = trans;
+    return o;
+  };
+  auto L_at = [&](int r0, int c0, int trans = 0) {
+    Operand o = opnd(Linv, nn, n, kIdxSegRow);
+    o.row0 = r0;
+    o.col0 = c0;
+    o.trans = trans;
+    return o;
+  };
+  BigDiagArgs a{};
+  a.D = opnd(WD, nn, n, kIdxSeg);
+  a.Linv = opnd(Linv, nn, n, kIdxSegRow);
+  a.seps = c.seps;
+  a.N = c.N;
+  a.base_mode = c.base_mode;
+  a.j = j;
+  a.n = n;
+  a.level = level;
+  a.k0 = c.k0;
+  a.err = err;
+  cudaError_t e;
+  for (int kb = 0; kb < NB; ++kb) {
+    a.kb = kb;
+    big_diag_potrf_kernel<<<(unsigned)c.K, 128, 0, c.s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (kb + 1 == NB) break;
+    const int r0 = (kb + 1) * BT, rows = n - r0;
+    e = big_gemm(c, j, kActAll, D_at(r0, kb * BT), L_at(kb * BT, kb * BT, 1), D_at(r0, kb * BT), D_at(r0, kb * BT),
+                 rows, BT, BT, 1.0, 0.0);
+    if (e != cudaSuccess) return e;
+    e = big_gemm(c, j, kActAll, D_at(r0, kb * BT), D_at(r0, kb * BT, 1), D_at(r0, r0), D_at(r0, r0), rows, rows, BT,
+                 -1.0, 1.0, 1);
+    if (e != cudaSuccess) return e;
+  }
+  for (int ib = 1; ib < NB; ++ib) {
+    const int w = ib * BT;
+    // T = L[ib][0:ib] Linv[0:ib][0:ib] (Linv lower: tri 4), stored transposed at D[0:w][w:w+64]
+    e = big_gemm(c, j, kActAll, D_at(w, 0), L_at(0, 0), D_at(0, w), D_at(0, w), BT, w, w, 1.0, 0.0, 0, 4, 1);
+    if (e != cudaSuccess) return e;
+    // Linv[ib][0:ib] = -Linv_ii T  (Linv_ii lower: tri 2)
+    e = big_gemm(c, j, kActAll, L_at(w, w), D_at(0, w, 1), L_at(w, 0), L_at(w, 0), BT, w, BT, -1.0, 0.0, 0, 2);
+    if (e != cudaSuccess) return e;
+  }
+  if (NB > 1) {
+    big_zero_upper_kernel<<<dim3((unsigned)(NB * (NB - 1) / 2), (unsigned)c.K), 256, 0, c.s>>>(a);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
+// big_potrf_seq (batched tile launches) vs big_potrf_kernel (one CTA / cluster per block);
+// BTD_BIG_SEQ=0 / 1 forces one.
+bool big_seq_potrf(int n, int K) {
+  static int env = -2;
+  if (env == -2) {
+    const char* v = getenv("BTD_BIG_SEQ");
+    env = !v ? -1 : (v[0] == '0' ? 0 : 1);
+  }
+  if (env >= 0) return env == 1;
+  // measured: the per-launch cost of the k = 64 tile GEMMs loses below n = 1024 (cfg4 factor
+  // 38.6 vs 33.3 ms, n = 512 53 vs 47 ms) and wins at n = 1024 (111 vs 129 ms)
+  return n >= 1024;
+}
+
 // One level (coupled) or the base (base_mode) of the tiled factorization.
 cudaError_t big_factor_level(const BigCtx& c, int level, int Jmax, int n, const double* diag, const double* sub,
                              double* Linv, double* Lsub, double* Sl, double* Sr, double* Ssub, char* ws,
@@ -594,7 +674,9 @@ cudaError_t big_factor_level(const BigCtx& c, int level, int Jmax, int n, const 
   const Operand oLinvT = opnd(Linv, nn, n, kIdxSegRow, 0, 0, 1);
   const Operand oL1 = opnd(Lsub, nn, n, kIdxSegRow), oL1t = opnd(Lsub, nn, n, kIdxSegRow, 0, 0, 1);
   for (int j = 0; j < Jmax; ++j) {
-    {
+    if (big_seq_potrf(n, c.K)) {
+      BIG_CHECK(big_potrf_seq(c, level, j, n, WD, Linv, err));
+    } else {
       BigPotrfArgs a{};
       a.D = oWD;
       a.Linv = oLinv;
