@@ -211,11 +211,13 @@ def device_bytes(num_blocks: int, block_size: int, num_columns: int = 1, config=
     return int(arenas + pb.value + max(sb.value, vb.value))
 
 
-def bench_sweep(shapes, num_columns: int = 1, runs: int = 3, warmup: int = 1, seed: int = 0,
+def bench_sweep(shapes, num_columns: int = 1, runs: int = 3, warmup: int = 2, seed: int = 0,
                 config=None) -> list[BenchRow]:
     """The reference's ``bench`` sweep (bt/cli.py:151-186) on the GPU: for every (N, n), the seeded
     reference instance is generated, moved to the device, and factor / solve are timed with CUDA
-    events (mean of ``runs`` after ``warmup``); the residual comes from the fused GPU kernel."""
+    events (mean of ``runs`` after ``warmup``; two warm-ups by default, because repeated
+    factorizations alternate between two workspace address sets and each set's first call captures
+    its CUDA graph); the residual comes from the fused GPU kernel."""
     import torch
     from .core import BlockTridiagonalMatrix
     from .schur import recursive_factorize, recursive_solve
