@@ -19,6 +19,7 @@
 #include "btd_factor3.cuh"
 #include "btd_solve.cuh"
 #include "btd_solve2.cuh"
+#include "btd_solve3.cuh"
 #include "btd_big.cuh"
 #include "btd_spmv.cuh"
 #include "btd_small.cuh"
@@ -741,6 +742,41 @@ cudaError_t big_factor_level(const BigCtx& c, int level, int Jmax, int n, const 
 }
 
 // One level pass of the tiled solve.  mode: down (fold), up (boundary + solution), base.
+// n > 64 with d <= 4 on a level with many segments: solve_wide_kernel (btd_solve3.cuh), one CTA
+// per segment streaming the blocks, instead of tile GEMMs that would fill d of 64 output columns.
+// Narrow levels and the serial base keep the GEMM path (one CTA per segment would stream whole
+// blocks through a single SM).  BTD_WIDE_SOLVE=0 disables.
+bool use_wide_solve(int n, int d, int64_t K) {
+  static int env = -1;
+  if (env < 0) {
+    const char* v = getenv("BTD_WIDE_SOLVE");
+    env = (v && v[0] == '0') ? 0 : 1;
+  }
+  // blocks of <= 128 KB (n <= 128) stream fast enough through one SM even on narrow levels and
+  // the serial base; n = 192, 256 only when the level has many segments
+  return env == 1 && d <= 4 && (n <= 128 || (n <= 256 && K >= 64));
+}
+
+template <int DC>
+cudaError_t launch_wide_dc(const btd::SolveArgs& a, cudaStream_t s) {
+  const size_t smem = (size_t)5 * a.n * DC * sizeof(double);
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(btd::solve_wide_kernel<DC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  dim3 grid((unsigned)(a.mode == btd::kSolveBase ? 1 : a.K), (unsigned)((a.d + DC - 1) / DC));
+  btd::solve_wide_kernel<DC><<<grid, btd::kWideThreads, smem, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wide(const btd::SolveArgs& a, cudaStream_t s) {
+  if (a.d == 1) return launch_wide_dc<1>(a, s);
+  if (a.d == 2) return launch_wide_dc<2>(a, s);
+  return launch_wide_dc<4>(a, s);
+}
+
 cudaError_t big_solve_level(const BigCtx& c, int mode, int Jmax, int n, int d, const double* rhs, const double* Linv,
                             const double* Lsub, double* x, const double* xsep, double* fl, double* fr, double* Tws,
                             double* Uws) {
@@ -1497,8 +1533,26 @@ static int enqueue_solve(const btd_hierarchy* h, const double* rhs, double* x, i
       const int* sp = (const int*)(pers + lp.off_seps);
       BigCtx c{sp, lp.N, 0, (int)lp.K, err, stream};
       set_lengths(c, lp);
-      e = big_solve_level(c, btd::kSolveDown, jmax, n, dd, rhs_l[l], (const double*)(pers + lp.off_linv),
-                          (const double*)(pers + lp.off_lsub), x_l[l], nullptr, rhs_l[l + 1], fr_l[l], Tws, Uws);
+      if (use_wide_solve(n, dd, lp.K)) {
+        btd::SolveArgs a{};
+        a.rhs = rhs_l[l];
+        a.Linv = (const double*)(pers + lp.off_linv);
+        a.Lsub = (const double*)(pers + lp.off_lsub);
+        a.seps = sp;
+        a.x = x_l[l];
+        a.fl = rhs_l[l + 1];
+        a.fr = fr_l[l];
+        a.N = lp.N;
+        a.n = n;
+        a.d = dd;
+        a.K = (int)lp.K;
+        a.mode = btd::kSolveDown;
+        a.err = err;
+        e = launch_wide(a, stream);
+      } else {
+        e = big_solve_level(c, btd::kSolveDown, jmax, n, dd, rhs_l[l], (const double*)(pers + lp.off_linv),
+                            (const double*)(pers + lp.off_lsub), x_l[l], nullptr, rhs_l[l + 1], fr_l[l], Tws, Uws);
+      }
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(big down)");
       btd::assemble_separator_rhs_kernel<<<flat_grid(lp.P * h->n * d), 256, 0, stream>>>(rhs_l[l], sp, rhs_l[l + 1], fr_l[l],
                                                                               (int)lp.K, n, dd, err); g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -1517,8 +1571,23 @@ static int enqueue_solve(const btd_hierarchy* h, const double* rhs, double* x, i
       c.jreg = c.jtail = (int)h->base_N;
       c.part = part;
       c.part_doubles = big_solve_part_doubles(h->n, d);
-      e = big_solve_level(c, btd::kSolveBase, (int)h->base_N, n, dd, rhs_l[L], (const double*)(pers + h->off_base_linv),
-                          (const double*)(pers + h->off_base_lsub), x_l[L], nullptr, nullptr, nullptr, Tws, Uws);
+      if (use_wide_solve(n, dd, 1)) {
+        btd::SolveArgs a{};
+        a.rhs = rhs_l[L];
+        a.Linv = (const double*)(pers + h->off_base_linv);
+        a.Lsub = (const double*)(pers + h->off_base_lsub);
+        a.x = x_l[L];
+        a.N = h->base_N;
+        a.n = n;
+        a.d = dd;
+        a.K = 1;
+        a.mode = btd::kSolveBase;
+        a.err = err;
+        e = launch_wide(a, stream);
+      } else {
+        e = big_solve_level(c, btd::kSolveBase, (int)h->base_N, n, dd, rhs_l[L], (const double*)(pers + h->off_base_linv),
+                            (const double*)(pers + h->off_base_lsub), x_l[L], nullptr, nullptr, nullptr, Tws, Uws);
+      }
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(big base)");
     }
     for (size_t l = L; l-- > 0;) {
@@ -1528,6 +1597,24 @@ static int enqueue_solve(const btd_hierarchy* h, const double* rhs, double* x, i
       const int* sp = (const int*)(pers + lp.off_seps);
       BigCtx c{sp, lp.N, 0, (int)lp.K, err, stream};
       set_lengths(c, lp);
+      if (use_wide_solve(n, dd, lp.K)) {
+        btd::SolveArgs a{};
+        a.rhs = rhs_l[l];
+        a.Linv = (const double*)(pers + lp.off_linv);
+        a.Lsub = (const double*)(pers + lp.off_lsub);
+        a.seps = sp;
+        a.xsep = x_l[l + 1];
+        a.x = x_l[l];
+        a.N = lp.N;
+        a.n = n;
+        a.d = dd;
+        a.K = (int)lp.K;
+        a.mode = btd::kSolveUp;
+        a.err = err;
+        e = launch_wide(a, stream);
+        if (e != cudaSuccess) return cuda_fail(st, e, "btd_solve(wide up)");
+        continue;
+      }
       const long long nn = (long long)n * n, ps = (long long)n * dd;
       const double* Ls = (const double*)(pers + lp.off_lsub);
       // boundary-modified rhs: b_0 -= C_L x_L ; b_last -= C_R^T x_R

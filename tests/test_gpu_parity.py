@@ -75,6 +75,8 @@ SWEEP = [  # (N, n, d, crossover, rho)
     (20, 128, 2, 4, 3), (70, 256, 3, 8, 8), (9, 192, 1, 2, 2), (3, 128, 65, 1, 1), (50, 256, 70, 64, 8),
     # n > 64 and not a multiple of 64: padded to the next multiple of 64 (schur._padded_size)
     (90, 80, 2, 8, 4), (40, 100, 1, 64, 8), (25, 65, 3, 4, 2), (12, 150, 2, 2, 2),
+    # n > 64, d <= 4, >= 64 segments per level: solve_wide_kernel (btd_solve3.cuh)
+    (700, 128, 3, 64, 8), (600, 192, 1, 64, 8), (650, 100, 2, 64, 8),
 ]
 
 
