@@ -50,16 +50,30 @@ template <int DC, bool LOWER>
 __device__ __forceinline__ void wide_mv_cols(const double* __restrict__ M, int n, const double* x, double* y, double sign,
                                              bool accumulate) {
   for (int c = threadIdx.x; c < n; c += kWideThreads) {
-    double s[DC];
+    double s[4][DC];  // four interleaved partial sums: the row loop is a latency chain otherwise
 #pragma unroll
-    for (int q = 0; q < DC; ++q) s[q] = 0.0;
-    for (int r = LOWER ? c : 0; r < n; ++r) {
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int q = 0; q < DC; ++q) s[i][q] = 0.0;
+    int r = LOWER ? c : 0;
+    for (; r + 3 < n; r += 4) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double v = __ldg(M + (size_t)(r + i) * n + c);
+#pragma unroll
+        for (int q = 0; q < DC; ++q) s[i][q] = fma(v, x[(r + i) * DC + q], s[i][q]);
+      }
+    }
+    for (; r < n; ++r) {
       const double v = __ldg(M + (size_t)r * n + c);
 #pragma unroll
-      for (int q = 0; q < DC; ++q) s[q] = fma(v, x[r * DC + q], s[q]);
+      for (int q = 0; q < DC; ++q) s[0][q] = fma(v, x[r * DC + q], s[0][q]);
     }
 #pragma unroll
-    for (int q = 0; q < DC; ++q) y[c * DC + q] = accumulate ? fma(sign, s[q], y[c * DC + q]) : sign * s[q];
+    for (int q = 0; q < DC; ++q) {
+      const double t = (s[0][q] + s[1][q]) + (s[2][q] + s[3][q]);
+      y[c * DC + q] = accumulate ? fma(sign, t, y[c * DC + q]) : sign * t;
+    }
   }
 }
 
