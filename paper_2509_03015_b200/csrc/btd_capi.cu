@@ -1155,7 +1155,7 @@ cudaError_t copy_diag_h2d(double* dev, const double* host, int64_t b0, int64_t n
   const size_t nn = (size_t)n * n;
   if (nb <= 0) return cudaSuccess;
   int G = n >= 64 ? 4 : n >= 32 ? 2 : 1;
-  if (env != 99) G = env <= 0 ? 1 : std::min<int>(env, G);
+  if (env != 99) G = env <= 0 ? 1 : std::min<int>(env, (int)n);
   while (G > 1 && n % G) --G;
   if (G <= 1)
     return cudaMemcpyAsync(dev + b0 * nn, host + b0 * nn, (size_t)nb * nn * sizeof(double), cudaMemcpyHostToDevice, s);
