@@ -867,9 +867,12 @@ bool graphs_enabled() {
   return v == 1;
 }
 
+// The launch sequence is recorded on a private capture stream (the caller's stream may be the
+// legacy default stream, which cannot be captured -- torch's default) and the instantiated graph is
+// launched into the caller's stream, so stream order is what the caller sees either way.
 template <class F>
 int run_graphed(GraphKey key, cudaStream_t stream, btd_status* st, F&& enqueue) {
-  if (!graphs_enabled()) return enqueue();
+  if (!graphs_enabled()) return enqueue(stream);
   int dev = 0;
   cudaGetDevice(&dev);
   key.device = dev;
@@ -884,31 +887,40 @@ int run_graphed(GraphKey key, cudaStream_t stream, btd_status* st, F&& enqueue) 
       return BTD_OK;
     }
   }
-  cudaStreamCaptureStatus cs;
-  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
-    return enqueue();  // the caller is capturing already: just record into its graph
-  const long long before = g_launches.load();
-  if (cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (stream && (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)) {
     cudaGetLastError();
-    return enqueue();
+    return enqueue(stream);  // the caller is capturing already: just record into its graph
   }
-  const int rc = enqueue();
+  cudaStream_t cap = nullptr;
+  if (cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    return enqueue(stream);
+  }
+  const long long before = g_launches.load();
+  if (cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    cudaStreamDestroy(cap);
+    return enqueue(stream);
+  }
+  const int rc = enqueue(cap);
   cudaGraph_t graph = nullptr;
-  cudaError_t e = cudaStreamEndCapture(stream, &graph);
+  cudaError_t e = cudaStreamEndCapture(cap, &graph);
+  cudaStreamDestroy(cap);
   const long long launches = g_launches.load() - before;
   g_launches.fetch_sub(launches, std::memory_order_relaxed);  // counted when the graph runs
   if (rc != BTD_OK || e != cudaSuccess || !graph) {
     if (graph) cudaGraphDestroy(graph);
     cudaGetLastError();
     clear_status(st);
-    return enqueue();  // nothing ran during the failed capture: run the sequence directly
+    return enqueue(stream);  // nothing ran during the failed capture: run the sequence directly
   }
   cudaGraphExec_t exec = nullptr;
   e = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
   if (e != cudaSuccess) {
     cudaGetLastError();
-    return enqueue();
+    return enqueue(stream);
   }
   e = cudaGraphLaunch(exec, stream);
   if (e != cudaSuccess) {
@@ -1421,8 +1433,8 @@ static int factorize_impl(btd_hierarchy* h, const double* diag, const double* su
     const GraphKey key{0, h->N, h->n, h->cfg.crossover, h->cfg.segment_length, h->cfg.max_levels,
                        h->cfg.auto_crossover, (int64_t)h->levels.size(), h->partial ? 1 : 0,
                        {diag, sub, pers, scr, red_diag, red_sub, nullptr}};
-    rc = run_graphed(key, stream, st, [&]() {
-      return enqueue_factor(h, diag, sub, pers, scr, stream, st, red_diag, red_sub, nullptr);
+    rc = run_graphed(key, stream, st, [&](cudaStream_t sq) {
+      return enqueue_factor(h, diag, sub, pers, scr, sq, st, red_diag, red_sub, nullptr);
     });
   }
   if (rc != BTD_OK) return rc;
@@ -1725,8 +1737,8 @@ static int solve_impl(const btd_hierarchy* h, const double* rhs, double* x, int6
   const GraphKey key{1 + phase, h->N, h->n, h->cfg.crossover, h->cfg.segment_length, h->cfg.max_levels,
                      h->cfg.auto_crossover, (int64_t)h->levels.size(), d,
                      {h->persistent, rhs, x, scratch, red_in, red_out, (const void*)(intptr_t)h->partial}};
-  return run_graphed(key, stream, st, [&]() {
-    return enqueue_solve(h, rhs, x, d, scratch, stream, st, phase, red_in, red_out);
+  return run_graphed(key, stream, st, [&](cudaStream_t sq) {
+    return enqueue_solve(h, rhs, x, d, scratch, sq, st, phase, red_in, red_out);
   });
 }
 
