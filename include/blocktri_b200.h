@@ -185,6 +185,8 @@ long long btd_launch_count(void);
  * buffers.  Enabled by default (environment BTD_GRAPHS=0 disables); returns the previous setting.
  * Disabling drops the cached graphs. */
 int btd_set_graphs(int32_t enable);
+/* Process-wide count of factor / solve calls served by replaying a cached graph. */
+long long btd_graph_replays(void);
 
 #ifdef __cplusplus
 }

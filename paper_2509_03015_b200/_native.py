@@ -38,7 +38,7 @@ EXPORTED_SYMBOLS = (
     "btd_solve_workspace", "btd_solve", "btd_level_factor", "btd_profile_kernels", "btd_kernel_times",
     "btd_create_partial", "btd_reduced_size", "btd_factorize_partial", "btd_solve_down", "btd_solve_up", "btd_launch_count",
     "btd_matmul", "btd_residual_workspace", "btd_residual_norms", "btd_factorize_from_host",
-    "btd_kalman_workspace", "btd_kalman_normal_equations", "btd_set_graphs",
+    "btd_kalman_workspace", "btd_kalman_normal_equations", "btd_set_graphs", "btd_graph_replays",
 )
 
 
@@ -110,6 +110,7 @@ def lib() -> ctypes.CDLL:
         L.btd_kernel_times.argtypes = [c_vp, P(ctypes.c_float), c_i64, P(c_i64)]
         L.btd_launch_count.argtypes = []
         L.btd_set_graphs.argtypes = [c_i32]
+        L.btd_graph_replays.argtypes = []
         L.btd_factorize_from_host.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, P(BtdStatus)]
         L.btd_kalman_workspace.argtypes = [c_i64, c_i64, P(c_sz)]
         L.btd_kalman_normal_equations.argtypes = [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32,
@@ -118,8 +119,10 @@ def lib() -> ctypes.CDLL:
         L.btd_residual_workspace.argtypes = [c_i64, c_i64, c_i64, P(c_sz)]
         L.btd_residual_norms.argtypes = [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, P(BtdStatus)]
         for name in EXPORTED_SYMBOLS:
-            if name not in ("btd_version", "btd_default_config", "btd_destroy", "btd_launch_count"):
+            if name not in ("btd_version", "btd_default_config", "btd_destroy", "btd_launch_count",
+                            "btd_graph_replays"):
                 getattr(L, name).restype = ctypes.c_int
         L.btd_launch_count.restype = ctypes.c_longlong
+        L.btd_graph_replays.restype = ctypes.c_longlong
         _lib = L
         return L

@@ -853,6 +853,7 @@ struct GraphEntry {
 std::mutex g_graph_mu;
 std::map<GraphKey, GraphEntry> g_graphs;
 unsigned long long g_graph_clock = 0;
+std::atomic<long long> g_graph_replays{0};  // graph launches served from the cache (btd_graph_replays)
 constexpr size_t kMaxGraphs = 32;
 
 std::atomic<int> g_graphs_on{-1};  // -1: not read from BTD_GRAPHS yet
@@ -884,6 +885,7 @@ int run_graphed(GraphKey key, cudaStream_t stream, btd_status* st, F&& enqueue) 
       cudaError_t e = cudaGraphLaunch(it->second.exec, stream);
       if (e != cudaSuccess) return cuda_fail(st, e, "cudaGraphLaunch");
       g_launches.fetch_add(it->second.launches, std::memory_order_relaxed);
+      g_graph_replays.fetch_add(1, std::memory_order_relaxed);
       return BTD_OK;
     }
   }
@@ -1827,6 +1829,8 @@ int btd_kernel_times(const btd_hierarchy* h, float* ms_out, int64_t cap, int64_t
   }
   return BTD_OK;
 }
+
+long long btd_graph_replays(void) { return g_graph_replays.load(std::memory_order_relaxed); }
 
 int btd_set_graphs(int32_t enable) {
   const int prev = graphs_enabled() ? 1 : 0;

@@ -93,3 +93,16 @@ def test_graph_replay_reports_npd_coordinates():
     X = pkg.recursive_solve(h, pkg.BlockRhs(torch.from_numpy(B.blocks).cuda()))
     _, rres = pkg.residual_report(dA, X, pkg.BlockRhs(torch.from_numpy(B.blocks).cuda()))
     assert rres <= 1e-12
+
+
+def test_graphs_replay_on_the_default_stream():
+    """torch's default stream is the legacy NULL stream (not capturable): the library records on a
+    private stream and replays into the caller's, so steady-state calls are graph replays."""
+    A, B = pkg.generate_spd_btd(3000, 64, 1, seed=6)
+    dA, dB = _device(A, B)
+    for _ in range(3):  # two alternating workspace address sets get captured
+        _run(dA, dB)
+    L = _native.lib()
+    r0 = L.btd_graph_replays()
+    _run(dA, dB)
+    assert L.btd_graph_replays() - r0 == 2  # the factorization and the solve
