@@ -478,7 +478,12 @@ cudaError_t big_gemm(const BigCtx& c, int j, int act, btd::Operand A, btd::Opera
   // split-k when the grid is far too small for the machine (the serial base: one segment) and k is
   // long enough to pay for the extra reduce launch (measured: a loss at k = 128/256, a gain at 1024)
   g.ksplit = 1;
-  if (c.part && c.K == 1 && k >= 512) {
+  static int mink = -1;
+  if (mink < 0) {
+    const char* v = getenv("BTD_SPLITK_MINK");  // A/B knob
+    mink = v ? atoi(v) : 512;
+  }
+  if (c.part && c.K == 1 && k >= mink) {
     static int sms = 0;
     if (!sms) {
       int dev = 0;
