@@ -5,7 +5,9 @@
 // bandwidth: every block the sweep needs is streamed global->shared by a TMA producer warp through
 // an mbarrier ring that runs ahead of the arithmetic across segment boundaries, and the inverse diagonal
 // factors are read in packed lower-triangular form (n(n+1)/2 instead of n^2 doubles).  The
-// backward sweep re-reads a segment's blocks right after the forward sweep, so they come from L2.
+// backward sweep re-reads a segment's blocks right after the forward sweep, so they come from L2
+// (forward loads carry an L2 evict_last hint, last uses evict_first: with two segments in flight
+// per SM on wide levels the re-read window is ~120 MB, close to the L2 size).
 //
 // Step streams (one step = at most one full n x n block + one packed block + one n x d panel):
 //   down : F_0 .. F_{J-1}, B_{J-1}, CR, B_{J-2} .. B_0, CL
@@ -59,7 +61,8 @@ enum StepKind : int { kStepF = 0, kStepB = 1, kStepCL = 2, kStepCR = 3, kStepNon
 // Producer/consumer version (n == NT, n even): warp NCW (the last warp) streams the step blocks
 // with TMA 1D bulk copies (cp.async.bulk, SASS UBLKCP) into a ring of STAGES slots guarded by
 // full/empty mbarriers, running ahead across segment boundaries; warps [0, NCW) compute with
-// vectorised, bank-rotated shared-memory mat-vecs.  Consumer barriers are named barrier 1.
+// vectorised, conflict-free shared-memory mat-vecs (two per step, one named barrier after each;
+// each warp releases a slot on its own).  Consumer barriers are named barrier 1.
 // ============================================================================================
 template <int NT>
 __device__ __forceinline__ void csync() {
