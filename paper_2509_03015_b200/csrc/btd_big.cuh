@@ -67,6 +67,7 @@ struct GemmArgs {
   const int* seps;
   long long N;
   int base_mode, j, act;
+  int level;             // factor level of the launch (INT_MAX: a solve launch, any error stops it)
   int m, n, k;           // op(A) m x k, op(B) k x n
   double alpha, beta;    // Cout = alpha op(A) op(B) + beta Cin   (beta == 0: Cin unused)
   int lower_only;        // skip tiles strictly above the diagonal (symmetric outputs)
@@ -175,8 +176,10 @@ __device__ __forceinline__ void gemm_tile_pipelined(double (&acc)[2][4][2], cons
 
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(BTHREADS) bt_gemm_kernel(GemmArgs g) {
-  if (error_raised(g.err)) return;
   const int k = g.k0 + blockIdx.y;
+  // skip only when a recorded failure can no longer be superseded by this (step, member): a lower
+  // member failing at a later 64-column tile of the same step must still be found
+  if (npd_superseded(g.err, g.level, g.j, k)) return;
   int J;
   if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, g.act, J)) return;
   const int ks = g.ksplit > 1 ? g.ksplit : 1;
@@ -239,8 +242,8 @@ __global__ void __launch_bounds__(BTHREADS) bt_gemm_kernel(GemmArgs g) {
 // Split-k epilogue: C = alpha * (sum of the partials in split order) + beta * Cin, per 64 x 64 tile
 // (deterministic: fixed summation order).  grid.x = tiles, blockIdx.y = segment (as the GEMM).
 __global__ void __launch_bounds__(BTHREADS) bt_gemm_reduce_kernel(GemmArgs g) {
-  if (error_raised(g.err)) return;
   const int k = g.k0 + blockIdx.y;
+  if (npd_superseded(g.err, g.level, g.j, k)) return;
   int J;
   if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, g.act, J)) return;
   const int tile = blockIdx.x, tm = tile / g.tiles_n, tn = tile % g.tiles_n;
@@ -281,8 +284,8 @@ struct BigDiagArgs {
 
 __global__ void __launch_bounds__(128) big_diag_potrf_kernel(BigDiagArgs g) {
   constexpr int LD = FactorShape<64>::LD;
-  if (error_raised(g.err)) return;
   const int k = g.k0 + blockIdx.x;
+  if (npd_superseded(g.err, g.level, g.j, k)) return;
   int J;
   if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, kActAll, J)) return;
   __shared__ __align__(16) double DL[BT * LD];
@@ -305,8 +308,8 @@ __global__ void __launch_bounds__(128) big_diag_potrf_kernel(BigDiagArgs g) {
 
 // zero the strict upper 64 x 64 tiles of every active segment's n x n Linv (grid.x = tile pairs)
 __global__ void big_zero_upper_kernel(BigDiagArgs g) {
-  if (error_raised(g.err)) return;
   const int k = g.k0 + blockIdx.y;
+  if (npd_superseded(g.err, g.level, g.j, k)) return;
   int J;
   if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, kActAll, J)) return;
   double* Li = const_cast<double*>(operand_ptr(g.Linv, g.seps, g.base_mode, k, g.j));
@@ -326,6 +329,7 @@ struct CopyArgs {
   const int* seps;
   long long N;
   int base_mode, j, act;
+  int level;       // as GemmArgs::level
   int rows, cols;  // of the destination
   int k0;          // first segment of this launch
   const DevErr* err;
@@ -333,8 +337,8 @@ struct CopyArgs {
 
 // dst[r][c] = src[r][c] (or src[c][r] when src.trans); blockIdx.y = segment
 __global__ void bt_copy_kernel(CopyArgs c) {
-  if (error_raised(c.err)) return;
   const int k = c.k0 + blockIdx.y;
+  if (npd_superseded(c.err, c.level, c.j, k)) return;
   int J;
   if (!segment_active(c.seps, c.base_mode, c.N, k, c.j, c.act, J)) return;
   const double* s = operand_ptr(c.src, c.seps, c.base_mode, k, c.j);
@@ -379,7 +383,7 @@ __global__ void __launch_bounds__(BTHREADS) big_potrf_kernel(BigPotrfArgs g) {
   // exits must be uniform over a cluster (cluster barriers follow): with csize > 1 a segment does
   // not skip on another segment's error (its own step-(j-1) failure was already reported, and a
   // later report can never supersede an earlier one)
-  if (C == 1 && error_raised(g.err)) return;
+  if (C == 1 && npd_superseded(g.err, g.level, g.j, k)) return;
   if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, kActAll, J)) return;
   extern __shared__ __align__(16) double sm[];
   double* DL = sm;             // 64 x LD diagonal tile (rank 0)

@@ -154,14 +154,62 @@ bool should_recurse(int64_t N, const btd_config& cfg) {
   return N > cfg.crossover;
 }
 
+// ---- per-device launch state --------------------------------------------------------------
+// The dynamic shared-memory attribute and the SM count are per device, and one process may drive
+// several GPUs from several threads: both are cached per (kernel, device) under a mutex.
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+int device_sms() {
+  static std::atomic<int> cache[kMaxDevices];
+  const int d = current_device();
+  int v = (d >= 0 && d < kMaxDevices) ? cache[d].load(std::memory_order_relaxed) : 0;
+  if (!v) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || v < 1) v = 148;
+    if (d >= 0 && d < kMaxDevices) cache[d].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+std::mutex g_attr_mu;
+std::map<std::pair<const void*, int>, int> g_smem_set;       // (kernel, device) -> configured bytes
+std::map<std::pair<const void*, int>, int> g_blocks_per_sm;  // (kernel, device) -> occupancy
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize >= smem for `fn` on the current device
+cudaError_t ensure_smem(const void* fn, size_t smem) {
+  if (smem <= 48 * 1024) return cudaSuccess;
+  const int d = current_device();
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  int& have = g_smem_set[{fn, d}];
+  if (have >= (int)smem) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) have = (int)smem;
+  return e;
+}
+
+// resident CTAs per SM of `fn` on the current device (after ensure_smem)
+int resident_blocks(const void* fn, int threads, size_t smem) {
+  const int d = current_device();
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  auto it = g_blocks_per_sm.find({fn, d});
+  if (it != g_blocks_per_sm.end()) return it->second;
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, threads, smem) != cudaSuccess || b < 1) {
+    cudaGetLastError();
+    b = 1;
+  }
+  g_blocks_per_sm[{fn, d}] = b;
+  return b;
+}
+
 // grid of a flattened grid-stride elementwise kernel (256 threads per CTA)
 unsigned flat_grid(int64_t elements) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = device_sms();
   const int64_t want = (elements + 255) / 256;
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 16));
 }
@@ -177,15 +225,9 @@ int pick_nt(int64_t n) {
 template <int NT>
 cudaError_t launch_factor(const btd::FactorArgs& a, unsigned grid, cudaStream_t s) {
   using S = btd::FactorShape<NT>;
-  static bool configured = false;
-  // BTD_ONE_CTA=1 (experiment): inflate the dynamic shared memory so only one CTA fits per SM
-  static const size_t smem = (getenv("BTD_ONE_CTA") != nullptr && NT == 64) ? (size_t)150 * 1024 : S::SMEM;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(btd::factor_level_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  constexpr size_t smem = S::SMEM;
+  cudaError_t e = ensure_smem((const void*)btd::factor_level_kernel<NT>, smem);
+  if (e != cudaSuccess) return e;
   btd::factor_level_kernel<NT><<<grid, S::NTHREADS, smem, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
@@ -194,47 +236,21 @@ cudaError_t launch_factor(const btd::FactorArgs& a, unsigned grid, cudaStream_t 
 // SM (and the base): its per-step latency is lower than factor_level_kernel's, but with one CTA
 // per SM it sustains less DMMA throughput on wide levels (measured: level 0 of cfg2 9.1 ms vs
 // 6.6 ms), where two factor_level_kernel CTAs per SM hide each other's pivot chains better.
-// BTD_STREAM=0 / 1 forces it off / on everywhere (A/B timing).
 bool use_stream(int nt, const btd::FactorArgs& a) {
-  static int env = -2;
-  if (env == -2) {
-    const char* v = getenv("BTD_STREAM");
-    env = !v ? -1 : (v[0] == '0' ? 0 : 1);
-  }
-  if (nt != 64 || env == 0) return false;
-  if (env == 1) return true;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return a.base || a.K <= sms;
+  if (nt != 64) return false;
+  return a.base || a.K <= device_sms();
 }
 
 cudaError_t launch_stream64(const btd::FactorArgs& a, unsigned grid, cudaStream_t s) {
   using SS = btd::StreamShape;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(btd::factor_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)SS::SMEM);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = ensure_smem((const void*)btd::factor_stream_kernel, SS::SMEM);
+  if (e != cudaSuccess) return e;
   btd::factor_stream_kernel<<<grid, SS::NTHREADS, SS::SMEM, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
-// Register-resident small-block kernel (btd_small.cuh) at NT = 8; BTD_SMALL=0 falls back to
-// factor_level_kernel<8> (A/B timing).
-bool use_small(int nt) {
-  static int env = -1;
-  if (env < 0) {
-    const char* v = getenv("BTD_SMALL");
-    env = (v && v[0] == '0') ? 0 : 1;
-  }
-  return env && nt == 8;
-}
+// Register-resident small-block kernel (btd_small.cuh) at NT = 8.
+bool use_small(int nt) { return nt == 8; }
 
 cudaError_t dispatch_factor(int nt, const btd::FactorArgs& a, unsigned grid, cudaStream_t s) {
   if (use_small(nt)) {
@@ -269,20 +285,10 @@ cudaError_t dispatch_solve_dc(const btd::SolveArgs& a, unsigned grid_x, cudaStre
 template <int NT, int DC, bool WIDE>
 cudaError_t launch_stream_v(const btd::SolveArgs& a, cudaStream_t s) {
   using T = btd::TmaShape<NT, DC, WIDE>;
-  static int blocks_per_sm = -1, sms = 0;
-  if (blocks_per_sm < 0) {
-    cudaError_t e = cudaFuncSetAttribute(btd::solve_tma_kernel<NT, DC, WIDE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, btd::solve_tma_kernel<NT, DC, WIDE>,
-                                                      T::NTHREADS, T::SMEM);
-    if (e != cudaSuccess) return e;
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
-  const long long cap = (long long)blocks_per_sm * sms;
+  const void* fn = (const void*)btd::solve_tma_kernel<NT, DC, WIDE>;
+  cudaError_t e = ensure_smem(fn, T::SMEM);
+  if (e != cudaSuccess) return e;
+  const long long cap = (long long)resident_blocks(fn, T::NTHREADS, T::SMEM) * device_sms();
   const unsigned gx = (unsigned)(a.K < cap ? a.K : cap);
   dim3 grid(gx, (unsigned)((a.d + DC - 1) / DC));
   btd::solve_tma_kernel<NT, DC, WIDE><<<grid, T::NTHREADS, T::SMEM, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -294,13 +300,7 @@ cudaError_t launch_stream_v(const btd::SolveArgs& a, cudaStream_t s) {
 template <int NT, int DC>
 cudaError_t launch_stream(const btd::SolveArgs& a, cudaStream_t s) {
   if constexpr (NT == 64 && DC == 1) {
-    static int sms = 0;
-    if (!sms) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    if (a.mode != btd::kSolveBase && a.K >= sms) return launch_stream_v<NT, DC, true>(a, s);
+    if (a.mode != btd::kSolveBase && a.K >= device_sms()) return launch_stream_v<NT, DC, true>(a, s);
   }
   return launch_stream_v<NT, DC, false>(a, s);
 }
@@ -409,6 +409,7 @@ struct BigCtx {
   int jreg = 0, jtail = 0;
   double* part = nullptr;  // split-k partials workspace (single-segment sequences: the serial base)
   size_t part_doubles = 0;
+  int level = INT_MAX;     // factor level (INT_MAX: solve sequences)
 };
 
 // split-k partials of the base solve's n x d products: 8 splits of ceil(n/64) x ceil(d/64) tiles
@@ -442,16 +443,14 @@ cudaError_t big_gemm(const BigCtx& c, int j, int act, btd::Operand A, btd::Opera
                      btd::Operand Cout, int m, int n, int k, double alpha, double beta, int lower = 0, int tri = 0,
                      int store_trans = 0) {
   if (!big_any_active(c, j, act)) return cudaSuccess;
-  static bool configured = false;
   const int smem = 4 * btd::GSTAGE * (int)sizeof(double);  // 2 stages x (A, B) tiles
-  if (!configured) {
+  {
     const void* fns[4] = {(const void*)btd::bt_gemm_kernel<false, false>, (const void*)btd::bt_gemm_kernel<false, true>,
                           (const void*)btd::bt_gemm_kernel<true, false>, (const void*)btd::bt_gemm_kernel<true, true>};
     for (const void* f : fns) {
-      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaError_t e = ensure_smem(f, smem);
       if (e != cudaSuccess) return e;
     }
-    configured = true;
   }
   btd::GemmArgs g{};
   g.A = A;
@@ -463,6 +462,7 @@ cudaError_t big_gemm(const BigCtx& c, int j, int act, btd::Operand A, btd::Opera
   g.base_mode = c.base_mode;
   g.j = j;
   g.act = act;
+  g.level = c.level;
   g.m = m;
   g.n = n;
   g.k = k;
@@ -478,18 +478,9 @@ cudaError_t big_gemm(const BigCtx& c, int j, int act, btd::Operand A, btd::Opera
   // split-k when the grid is far too small for the machine (the serial base: one segment) and k is
   // long enough to pay for the extra reduce launch (measured: a loss at k = 128/256, a gain at 1024)
   g.ksplit = 1;
-  static int mink = -1;
-  if (mink < 0) {
-    const char* v = getenv("BTD_SPLITK_MINK");  // A/B knob
-    mink = v ? atoi(v) : 512;
-  }
+  constexpr int mink = 512;
   if (c.part && c.K == 1 && k >= mink) {
-    static int sms = 0;
-    if (!sms) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = device_sms();
     int ks = std::min(8, std::max(1, sms / std::max(1, 2 * tiles)));
     ks = std::min(ks, std::max(1, k / btd::BK));
     while (ks > 1 && (size_t)tiles * ks * btd::BT * btd::BT > c.part_doubles) --ks;
@@ -519,6 +510,7 @@ cudaError_t big_copy(const BigCtx& c, int j, int act, btd::Operand src, btd::Ope
   a.base_mode = c.base_mode;
   a.j = j;
   a.act = act;
+  a.level = c.level;
   a.rows = rows;
   a.cols = cols;
   a.k0 = c.k0;
@@ -531,34 +523,16 @@ cudaError_t big_copy(const BigCtx& c, int j, int act, btd::Operand src, btd::Ope
 
 // CTAs per segment for big_potrf_kernel: 1 on wide levels; on narrow levels (the serial base, a
 // level with fewer segments than SMs) a cluster of up to 8 CTAs shares each block's tile GEMMs.
-// BTD_BIG_CLUSTER=<c> forces c (1 disables).
 int big_potrf_cluster(int K, int n, int sms) {
-  static int env = -2;
-  if (env == -2) {
-    const char* v = getenv("BTD_BIG_CLUSTER");
-    env = v ? std::max(1, std::min(8, atoi(v))) : -1;
-  }
   const int NB = n / btd::BT;
   const int maxc = std::max(1, std::min(8, NB * (NB - 1) / 2));  // more CTAs than trailing tiles idle
-  if (env > 0) return std::min(env, maxc);
   if (K >= sms) return 1;
   return std::max(1, std::min(maxc, sms / std::max(K, 1)));
 }
 
-// Split a wide n > 64 level into two half-level launch sequences on two streams (BTD_BIG_SPLIT=0
-// disables): each half's big_potrf_kernel (latency-bound, < 2 waves) overlaps the other half's
-// tile GEMMs.
-bool big_split_level(int64_t K) {
-  static int env = -1, sms = 0;
-  if (env < 0) {
-    const char* v = getenv("BTD_BIG_SPLIT");
-    env = (v && v[0] == '0') ? 0 : 1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return env == 1 && K >= 2 * (int64_t)sms;
-}
+// Split a wide n > 64 level into two half-level launch sequences on two streams: each half's
+// big_potrf_kernel (latency-bound, < 2 waves) overlaps the other half's tile GEMMs.
+bool big_split_level(int64_t K) { return K >= 2 * (int64_t)device_sms(); }
 
 cudaError_t ensure_aux(btd_hierarchy* h) {
   cudaError_t e = cudaSuccess;
@@ -634,15 +608,9 @@ cudaError_t big_potrf_seq(const BigCtx& c, int level, int j, int n, double* WD, 
   return e;
 }
 
-// big_potrf_seq (batched tile launches) vs big_potrf_kernel (one CTA / cluster per block);
-// BTD_BIG_SEQ=0 / 1 forces one.
+// big_potrf_seq (batched tile launches) vs big_potrf_kernel (one CTA / cluster per block)
 bool big_seq_potrf(int n, int K) {
-  static int env = -2;
-  if (env == -2) {
-    const char* v = getenv("BTD_BIG_SEQ");
-    env = !v ? -1 : (v[0] == '0' ? 0 : 1);
-  }
-  if (env >= 0) return env == 1;
+  (void)K;
   // measured: the per-launch cost of the k = 64 tile GEMMs loses below n = 1024 (cfg4 factor
   // 38.6 vs 33.3 ms, n = 512 53 vs 47 ms) and wins at n = 1024 (111 vs 129 ms)
   return n >= 1024;
@@ -695,16 +663,8 @@ cudaError_t big_factor_level(const BigCtx& c, int level, int Jmax, int n, const 
       a.k0 = c.k0;
       a.err = err;
       const int smem = (BT * FactorShape<64>::LD + 4 * GSTAGE) * (int)sizeof(double);
-      static bool conf = false;
-      static int sms = 0;
-      if (!conf) {
-        BIG_CHECK(cudaFuncSetAttribute(big_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        BIG_CHECK(cudaFuncSetAttribute(big_potrf_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        conf = true;
-      }
+      BIG_CHECK(ensure_smem((const void*)big_potrf_kernel, smem));
+      const int sms = device_sms();
       // a cluster of CTAs per segment when the level is too narrow to fill the SMs
       a.csize = big_potrf_cluster(c.K, n, sms);
       cudaLaunchConfig_t cfg{};
@@ -750,27 +710,18 @@ cudaError_t big_factor_level(const BigCtx& c, int level, int Jmax, int n, const 
 // n > 64 with d <= 4 on a level with many segments: solve_wide_kernel (btd_solve3.cuh), one CTA
 // per segment streaming the blocks, instead of tile GEMMs that would fill d of 64 output columns.
 // Narrow levels and the serial base keep the GEMM path (one CTA per segment would stream whole
-// blocks through a single SM).  BTD_WIDE_SOLVE=0 disables.
+// blocks through a single SM).
 bool use_wide_solve(int n, int d, int64_t K) {
-  static int env = -1;
-  if (env < 0) {
-    const char* v = getenv("BTD_WIDE_SOLVE");
-    env = (v && v[0] == '0') ? 0 : 1;
-  }
   // blocks of <= 128 KB (n <= 128) stream fast enough through one SM even on narrow levels and
   // the serial base; n = 192, 256 only when the level has many segments
-  return env == 1 && d <= 4 && (n <= 128 || (n <= 256 && K >= 64));
+  return d <= 4 && (n <= 128 || (n <= 256 && K >= 64));
 }
 
 template <int DC>
 cudaError_t launch_wide_dc(const btd::SolveArgs& a, cudaStream_t s) {
   const size_t smem = (size_t)5 * a.n * DC * sizeof(double);
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(btd::solve_wide_kernel<DC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  cudaError_t e = ensure_smem((const void*)btd::solve_wide_kernel<DC>, smem);
+  if (e != cudaSuccess) return e;
   dim3 grid((unsigned)(a.mode == btd::kSolveBase ? 1 : a.K), (unsigned)((a.d + DC - 1) / DC));
   btd::solve_wide_kernel<DC><<<grid, btd::kWideThreads, smem, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
@@ -1164,17 +1115,11 @@ struct HostSrc {
 // the rows are sent in G bands: band g (rows [g n/G, (g+1) n/G)) only its first (g+1) n/G columns,
 // the last band in full (G = 4 for n >= 64: 5/8 of the bytes; G = 2 for n >= 32: 3/4), one pitched
 // 3D copy per band with rows of >= 128 bytes.  The device copy's remaining upper triangle is never
-// read.  BTD_H2D_LOWER=0 sends whole blocks, BTD_H2D_LOWER=<G> forces G bands.
+// read.
 cudaError_t copy_diag_h2d(double* dev, const double* host, int64_t b0, int64_t nb, int64_t n, cudaStream_t s) {
-  static int env = -1;
-  if (env < 0) {
-    const char* v = getenv("BTD_H2D_LOWER");
-    env = v ? atoi(v) : 99;
-  }
   const size_t nn = (size_t)n * n;
   if (nb <= 0) return cudaSuccess;
   int G = n >= 64 ? 4 : n >= 32 ? 2 : 1;
-  if (env != 99) G = env <= 0 ? 1 : std::min<int>(env, (int)n);
   while (G > 1 && n % G) --G;
   if (G <= 1)
     return cudaMemcpyAsync(dev + b0 * nn, host + b0 * nn, (size_t)nb * nn * sizeof(double), cudaMemcpyHostToDevice, s);
@@ -1307,6 +1252,7 @@ static int enqueue_factor(btd_hierarchy* h, const double* diag, const double* su
       int jmax = 0;
       jmax = (int)lp.max_segment();
       BigCtx c{(const int*)(pers + lp.off_seps), lp.N, 0, (int)lp.K, err, stream};
+      c.level = (int)l;
       set_lengths(c, lp);
       double* next_diag = (double*)(scr + lp.off_next_diag);
       prof_mark(h, stream);
@@ -1350,6 +1296,7 @@ static int enqueue_factor(btd_hierarchy* h, const double* diag, const double* su
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize_partial(export)");
     } else if (!h->overflow) {
       BigCtx c{nullptr, h->base_N, 1, 1, err, stream};
+      c.level = (int)h->levels.size();
       c.jreg = c.jtail = (int)h->base_N;
       c.part = (double*)(scr + h->off_splitk);
       c.part_doubles = (size_t)8 * h->n * h->n;
@@ -1855,9 +1802,7 @@ long long btd_launch_count(void) { return g_launches.load(std::memory_order_rela
 // residual_report bt/report.py:20-38.
 // ---------------------------------------------------------------------------------------------
 static void spmv_grid(int64_t N, int64_t d, long long* rows_per_cta, unsigned* ctas, unsigned* ycols) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sms();
   const long long want = std::min<long long>(N, (long long)sms * 8);
   *rows_per_cta = (N + want - 1) / want;
   *ctas = (unsigned)((N + *rows_per_cta - 1) / *rows_per_cta);
@@ -1973,8 +1918,7 @@ int btd_kalman_normal_equations(int64_t horizon, int64_t n, int64_t m, const dou
   a.cross = cross;
   a.err = err;
   const size_t smem = btd::kalman_smem_doubles((int)n, (int)m, diag_r ? 0 : 1) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(btd::kalman_terms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  cudaError_t e = ensure_smem((const void*)btd::kalman_terms_kernel, smem);
   if (e != cudaSuccess) return cuda_fail(st, e, "btd_kalman_normal_equations(attr)");
   e = cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), s);
   if (e != cudaSuccess) return cuda_fail(st, e, "btd_kalman_normal_equations(init)");

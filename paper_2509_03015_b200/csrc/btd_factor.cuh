@@ -610,13 +610,7 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
     int fail = 0;
     if (in_a) fail = potrf_trtri<NT>(DL, &s_fail);
     if (NWB == 0) __syncthreads();  // single-warp CTA: group B work runs after the factor
-#ifdef BTD_EXP_B3
-    // experiment: keep the pivot-chain warp's SMSP (warp 4 = same scheduler as warp 0) free of
-    // group-B DMMA work during the Cholesky
-    constexpr int SKIPB = NWB >= 4 ? 1 : 0;
-#else
     constexpr int SKIPB = 0;
-#endif
     if (j > 0 && (NWB == 0 || (!in_a && wb >= SKIPB))) {
       const int w = NWB ? wb - SKIPB : 0, nw = NWB ? NWB - SKIPB : 1, nb = NWB ? (NWB - SKIPB) * 32 : 32;
       const int gt = NWB ? tid - (NWA + SKIPB) * 32 : tid;

@@ -202,11 +202,6 @@ __global__ void __launch_bounds__(StreamShape::NTHREADS, 1) factor_stream_kernel
       if (tid == 0) BTD_SPROF(11, tstep);
     } else {
       // ======== group B ========
-#ifdef BTD_EXP_SMSP0_IDLE
-      if ((warp & 3) == 0) {  // experiment: keep the chain's SMSP free (wrong results)
-        named_sync(kBarS, NB);
-      } else
-#endif
       {
       double X[8][2], G[8][2], Y[8][2];  // C fragments of the three owned tiles
       const bool has_x = coupled || !last;  // base: no X1 at the last row

@@ -11,6 +11,7 @@ allocates device memory through torch's caching allocator and maps status codes 
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from dataclasses import dataclass
 
@@ -196,13 +197,46 @@ def _pad_matrix(diag, sub, n: int, npad: int):
     return dp, sp
 
 
+@contextlib.contextmanager
+def _on_stream(device, stream):
+    """Run the body with ``device`` current and every torch op / native launch on ``stream``.
+
+    The stream waits for the caller's current stream on entry (inputs it produced) and the caller's
+    current stream waits for ``stream`` on exit (outputs and the freed scratch), so passing a
+    non-current stream is safe in both directions; the caching allocator attributes every
+    temporary to ``stream``."""
+    import torch
+    with torch.cuda.device(device):
+        cur = torch.cuda.current_stream(device)
+        s = stream if stream is not None else cur
+        if s != cur:
+            s.wait_stream(cur)
+        with torch.cuda.stream(s):
+            yield s
+        if s != cur:
+            cur.wait_stream(s)
+
+
+def _matrix_device(matrix: BlockTridiagonalMatrix):
+    import torch
+    if _is_torch(matrix.diag) and matrix.diag.device.type == "cuda":
+        return matrix.diag.device
+    return torch.device("cuda", torch.cuda.current_device())
+
+
 def recursive_factorize(matrix: BlockTridiagonalMatrix, config: RecursionConfig | None = None,
                         *, stream=None, profile: bool = False) -> FactorHierarchy:
     """Factor an SPD block-tridiagonal system for repeated solves (schur.py:289-318).
 
     Never mutates ``matrix``. Raises NotPositiveDefinite(pivot, level, member, block) with the
-    reference's level-local coordinates, LevelOverflow past ``max_levels``.
+    reference's level-local coordinates, LevelOverflow past ``max_levels``.  ``stream`` (optional)
+    is the CUDA stream the work is ordered on (default: the current stream of the matrix's device).
     """
+    with _on_stream(_matrix_device(matrix), stream) as s:
+        return _factorize_on(matrix, config, s, profile)
+
+
+def _factorize_on(matrix, config, s, profile):
     import torch
     cfg = config or RecursionConfig()
     L = _native.lib()
@@ -220,8 +254,8 @@ def recursive_factorize(matrix: BlockTridiagonalMatrix, config: RecursionConfig 
         if n != n_user:
             diag, sub = _pad_matrix(diag, sub, n_user, n)
     else:  # host-resident input: the C ABI overlaps the H2D copy with the level-0 elimination
-        diag = torch.empty((N, n, n), dtype=torch.float64, device="cuda")
-        sub = torch.empty((max(N - 1, 0), n, n), dtype=torch.float64, device="cuda")
+        diag = torch.empty((N, n, n), dtype=torch.float64, device=s.device)
+        sub = torch.empty((max(N - 1, 0), n, n), dtype=torch.float64, device=s.device)
     pers_b, scr_b = ctypes.c_size_t(), ctypes.c_size_t()
     L.btd_factor_workspace(handle, ctypes.byref(pers_b), ctypes.byref(scr_b))
     dev = diag.device
@@ -231,7 +265,6 @@ def recursive_factorize(matrix: BlockTridiagonalMatrix, config: RecursionConfig 
     native.padded = n  # kernel block size (> n_user when padded)
     if profile:
         L.btd_profile_kernels(handle, 1)
-    s = stream if stream is not None else torch.cuda.current_stream(dev)
     if host is None:
         rc = L.btd_factorize(handle, diag.data_ptr(), sub.data_ptr() if N > 1 else None, persistent.data_ptr(),
                              scratch.data_ptr(), ctypes.c_void_p(s.cuda_stream), 1, ctypes.byref(st))
@@ -257,8 +290,17 @@ def recursive_solve(hierarchy: FactorHierarchy, rhs: BlockRhs, *, stream=None) -
     """Solve against a stored factorization (schur.py:346-359).
 
     Neither the hierarchy nor ``rhs`` is mutated.  numpy rhs -> numpy solution (host round
-    trip); torch CUDA rhs -> torch CUDA solution (device resident).
+    trip); torch CUDA rhs -> torch CUDA solution (device resident).  ``stream`` as in
+    recursive_factorize.
     """
+    native = hierarchy._native
+    if native is None or not native.handle:
+        raise ValueError("hierarchy must be factorized before solving")
+    with _on_stream(native.device, stream) as s:
+        return _solve_on(hierarchy, rhs, s)
+
+
+def _solve_on(hierarchy, rhs, s):
     import torch
     if rhs.num_blocks != hierarchy.num_blocks or rhs.block_size != hierarchy.block_size:
         raise DimensionMismatch(
@@ -289,7 +331,6 @@ def recursive_solve(hierarchy: FactorHierarchy, rhs: BlockRhs, *, stream=None) -
     L.btd_solve_workspace(native.handle, d, ctypes.byref(scr_b))
     scratch = torch.empty(scr_b.value, dtype=torch.uint8, device=native.device)
     st = _native.BtdStatus()
-    s = stream if stream is not None else torch.cuda.current_stream(native.device)
     rc = L.btd_solve(native.handle, b.data_ptr(), x.data_ptr(), d, scratch.data_ptr(),
                      ctypes.c_void_p(s.cuda_stream), ctypes.byref(st))
     if rc != _native.BTD_OK:

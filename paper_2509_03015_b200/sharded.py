@@ -77,6 +77,19 @@ class ShardPlan:
     reduced_sizes: list = field(default_factory=list)   # P_g (separators of chunk g after L levels)
     offsets: list = field(default_factory=list)         # first reduced index of chunk g
     reduced_N: int = 0
+    crossover: int = 64         # RecursionConfig the cuts were planned for (the reduced sizes
+    rho: int = 8                # depend on segment_length; the solver config must match)
+
+    def config(self, config=None):
+        """The RecursionConfig of this plan; a given ``config`` must agree with it."""
+        from .schur import RecursionConfig
+        if config is None:
+            return RecursionConfig(crossover=self.crossover, segment_length=self.rho)
+        if config.segment_length != self.rho or config.crossover != self.crossover or config.auto_crossover:
+            raise ValueError(f"config (crossover={config.crossover}, segment_length={config.segment_length}, "
+                             f"auto={config.auto_crossover}) differs from the shard plan's "
+                             f"(crossover={self.crossover}, segment_length={self.rho})")
+        return config
 
     def chunk(self, g: int) -> tuple[int, int]:
         return self.cuts[g], self.cuts[g + 1]
@@ -104,7 +117,7 @@ def shard_plan(N: int, G: int, crossover: int = 64, rho: int = 8, L: int | None 
         cuts.append(c)
     cuts.append(N - 1)
     glob = _global_plans(N, L, rho)
-    plan = ShardPlan(N, G, L, cuts)
+    plan = ShardPlan(N, G, L, cuts, crossover=crossover, rho=rho)
     off = 0
     for g in range(G):
         a, b = cuts[g], cuts[g + 1]
@@ -171,6 +184,16 @@ def chunk_inputs(plan: ShardPlan, g: int, diag, sub, rhs=None):
 # ------------------------------------------------------------------------------------------
 # engines
 # ------------------------------------------------------------------------------------------
+def _on_device(fn):
+    """Run an engine method with the engine's device current (the C ABI launches on the current
+    device; the tensors live on ``self.device``)."""
+    def wrapped(self, *a, **k):
+        with self.torch.cuda.device(self.device):
+            return fn(self, *a, **k)
+    wrapped.__name__, wrapped.__doc__ = fn.__name__, fn.__doc__
+    return wrapped
+
+
 class CudaEngine:
     """Per-rank linear algebra on the sm_100a kernels (C ABI partial entry points)."""
 
@@ -182,6 +205,7 @@ class CudaEngine:
     def _cfg(self, cfg):
         return cfg._c()
 
+    @_on_device
     def factor_partial(self, diag, sub, L, cfg):
         torch = self.torch
         lib = _native.lib()
@@ -212,6 +236,7 @@ class CudaEngine:
         state = {"h": h, "pers": pers, "N": N, "n": n, "P": P.value}
         return state, rd, rs[:max(P.value - 1, 0)]
 
+    @_on_device
     def solve_down(self, state, rhs):
         torch = self.torch
         lib = _native.lib()
@@ -230,6 +255,7 @@ class CudaEngine:
             _raise_status(st, rc)
         return red
 
+    @_on_device
     def solve_up(self, state, rhs, red_x):
         torch = self.torch
         lib = _native.lib()
@@ -293,12 +319,14 @@ class ShardedSolver:
     def __init__(self, plan: ShardPlan, rank: int, comm, engine, config=None):
         from .schur import RecursionConfig
         self.plan, self.rank, self.comm, self.engine = plan, rank, comm, engine
-        self.cfg = config or RecursionConfig()
+        self.cfg = plan.config(config)
 
     def factorize(self, diag_chunk, sub_chunk):
         """diag/sub of this rank's chunk, ownership rule applied (see chunk_inputs)."""
         self.state, rd, rs = self.engine.factor_partial(diag_chunk, sub_chunk, self.plan.L, self.cfg)
         counts = self.plan.reduced_sizes
+        if rd.shape[0] != counts[self.rank]:
+            raise AssertionError(f"rank {self.rank}: reduced size {rd.shape[0]} != planned {counts[self.rank]}")
         diags = self.comm.all_gather_blocks(rd, counts)
         subs = self.comm.all_gather_blocks(rs, [max(c - 1, 0) for c in counts])
         D, S = assemble_reduced(self.plan, diags, subs)
@@ -317,12 +345,13 @@ class ShardedSolver:
 def run_sharded_local(plan: ShardPlan, engine, diag, sub, rhs, config=None):
     """All G ranks of the sharded algorithm played sequentially in one process (single-GPU check
     of the per-rank kernels and the assembly; the collective is the identity)."""
-    from .schur import RecursionConfig
-    cfg = config or RecursionConfig()
+    cfg = plan.config(config)
     states, rds, rss, rhs_c = [], [], [], []
     for g in range(plan.G):
         d, s, r = chunk_inputs(plan, g, diag, sub, rhs)
         st, rd, rs = engine.factor_partial(d, s, plan.L, cfg)
+        if rd.shape[0] != plan.reduced_sizes[g]:
+            raise AssertionError(f"chunk {g}: reduced size {rd.shape[0]} != planned {plan.reduced_sizes[g]}")
         states.append(st)
         rds.append(rd)
         rss.append(rs)

@@ -197,6 +197,11 @@ def test_host_input_npd_coordinates_match_device_path():
     (5000, 6, 8, 64, [(777, 2), (778, 0)]),        # n <= 8: factor_small_kernel
     (2000, 40, 3, 16, [(999, 17)]),                # n = 40 padded to 64
     (6000, 64, 8, 64, [(9 * 20, 3)]),              # a level-0 separator: fails at level 1
+    # n > 64 tiled path (two half-level streams at K = 333): two members failing in the same step
+    # at different 64-column tiles -> the lower member (tile 1) wins over the higher one (tile 0)
+    (3000, 128, 8, 64, [(9 * 3 + 1 + 2, 100), (9 * 5 + 1 + 2, 5)]),
+    # ... and an earlier step in the second half-level stream beats a later step in the first
+    (3000, 128, 8, 64, [(9 * 3 + 1 + 4, 5), (9 * 200 + 1 + 1, 70)]),
 ])
 def test_npd_coordinates_every_kernel_vs_oracle(N, n, rho, cross, bad):
     """A non-positive pivot reports the oracle's (pivot, level, member, block) -- the reference's
