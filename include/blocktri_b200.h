@@ -112,6 +112,14 @@ int btd_solve(const btd_hierarchy* h, const double* rhs, double* x, int64_t num_
 int btd_level_factor(const btd_hierarchy* h, int64_t level, double* linv_out, double* lsub_out,
                      void* stream, btd_status* st);
 
+/* Debug/introspection: the next-level (Schur complement) system produced by level `level`
+ * (compute_schur + new_btd, schur.py:156-193, core.py:205-211): P_l diagonal blocks (symmetric,
+ * mirrored from the lower triangle the kernels form) and P_l - 1 sub blocks, copied into caller
+ * device buffers.  `scratch` must be the factor scratch of the last btd_factorize on `h`, still
+ * unmodified (the Schur systems live there only until it is reused). */
+int btd_level_schur(const btd_hierarchy* h, int64_t level, const void* scratch, double* diag_out, double* sub_out,
+                    void* stream, btd_status* st);
+
 /* ---- Sharded (multi-GPU) building blocks, SURVEY.md §8e ----
  * The global chain is cut at level-L separators into contiguous chunks [a_g, b_g] (shared boundary
  * separators b_g = a_{g+1}); chunk g factors exactly `local_levels` levels of its own plan (which

@@ -323,6 +323,16 @@ def schur_level0(diag, sub, rho=8):
     return sd, ss
 
 
+def level_schur(diag, sub, level, crossover=64, rho=8):
+    """The Schur system level `level` hands to level + 1 (bt/schur.py:329-343 iterated)."""
+    cd, cs = diag, sub
+    for lvl in range(level + 1):
+        if not should_recurse(cd.shape[0], crossover, rho, False):
+            raise ValueError(f"level {lvl} does not recurse")
+        _, cd, cs = factor_level(cd, cs, rho, lvl)
+    return cd, cs
+
+
 # ------------------------------------------------------------------------------------------
 # dense checks: bt/oracle.py:26-74, bt/core.py:262-288, bt/report.py:20-38
 # ------------------------------------------------------------------------------------------

@@ -9,7 +9,7 @@ from .core import (BlockRhs, BlockTridiagonalMatrix, FactorHierarchy, PartitionP
                    new_btd, new_rhs)
 from .errors import (BadMagic, BtdFormatError, IoError, TruncatedPayload, VersionUnsupported, AsymmetricBlock, BlockTriError, DeviceError, DimensionMismatch, InvalidDimensions,
                      LevelOverflow, NotPositiveDefinite, SingularDiagonal)
-from .schur import (FactorLevel, RecursionConfig, level_factor, plan_partition, recursive_factorize,
+from .schur import (FactorLevel, RecursionConfig, level_factor, level_schur, plan_partition, recursive_factorize,
                     recursive_solve)
 from .synthgen import generate_spd_btd
 from .report import (SWEEPS, BenchRow, bench_sweep, btd_matmul, device_bytes, format_table, parse_sweep,
@@ -25,7 +25,7 @@ __all__ = [
     "AsymmetricBlock", "BlockRhs", "BlockTriError", "BlockTridiagonalMatrix", "DeviceError",
     "DimensionMismatch", "FactorHierarchy", "FactorLevel", "InvalidDimensions", "LevelOverflow",
     "NotPositiveDefinite", "PartitionPlan", "RecursionConfig", "SingularDiagonal", "btd_matmul",
-    "check_conformal", "generate_spd_btd", "level_factor", "new_btd", "new_rhs", "plan_partition",
+    "check_conformal", "generate_spd_btd", "level_factor", "level_schur", "new_btd", "new_rhs", "plan_partition",
     "recursive_factorize", "recursive_solve", "residual_report",
     "SWEEPS", "BenchRow", "bench_sweep", "device_bytes", "format_table", "parse_sweep", "time_call",
 ]

@@ -35,7 +35,7 @@ BTD_ERR_NOT_FACTORED = 7
 EXPORTED_SYMBOLS = (
     "btd_version", "btd_default_config", "btd_plan_separators", "btd_create", "btd_destroy",
     "btd_num_levels", "btd_level_info", "btd_factor_workspace", "btd_factorize", "btd_check",
-    "btd_solve_workspace", "btd_solve", "btd_level_factor", "btd_profile_kernels", "btd_kernel_times",
+    "btd_solve_workspace", "btd_solve", "btd_level_factor", "btd_level_schur", "btd_profile_kernels", "btd_kernel_times",
     "btd_create_partial", "btd_reduced_size", "btd_factorize_partial", "btd_solve_down", "btd_solve_up", "btd_launch_count",
     "btd_matmul", "btd_residual_workspace", "btd_residual_norms", "btd_factorize_from_host",
     "btd_kalman_workspace", "btd_kalman_normal_equations", "btd_set_graphs", "btd_graph_replays",
@@ -101,6 +101,7 @@ def lib() -> ctypes.CDLL:
         L.btd_solve_workspace.argtypes = [c_vp, c_i64, P(c_sz)]
         L.btd_solve.argtypes = [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, P(BtdStatus)]
         L.btd_level_factor.argtypes = [c_vp, c_i64, c_vp, c_vp, c_vp, P(BtdStatus)]
+        L.btd_level_schur.argtypes = [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, P(BtdStatus)]
         L.btd_profile_kernels.argtypes = [c_vp, c_i32]
         L.btd_create_partial.argtypes = [c_i64, c_i64, P(BtdConfig), c_i64, P(c_vp), P(BtdStatus)]
         L.btd_reduced_size.argtypes = [c_vp, P(c_i64)]

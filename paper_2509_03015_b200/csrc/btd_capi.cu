@@ -1752,6 +1752,28 @@ int btd_level_factor(const btd_hierarchy* h, int64_t level, double* linv_out, do
   return BTD_OK;
 }
 
+int btd_level_schur(const btd_hierarchy* h, int64_t level, const void* scratch, double* diag_out, double* sub_out,
+                    void* stream, btd_status* st) {
+  clear_status(st);
+  if (!h || !scratch || !diag_out || level < 0 || level >= (int64_t)h->levels.size() || !h->factored) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_level_schur: bad level, buffers or unfactored hierarchy");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  const LevelPlan& lp = h->levels[level];
+  const size_t bb = (size_t)h->n * h->n * sizeof(double);
+  const char* scr = (const char*)scratch;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(diag_out, scr + lp.off_next_diag, (size_t)lp.P * bb, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess && lp.P > 1 && sub_out)
+    e = cudaMemcpyAsync(sub_out, scr + lp.off_next_sub, (size_t)(lp.P - 1) * bb, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(st, e, "btd_level_schur(copy)");
+  btd::mirror_lower_kernel<<<flat_grid(lp.P * h->n * h->n), 256, 0, s>>>(diag_out, lp.P, (int)h->n);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(st, e, "btd_level_schur(mirror)");
+  return BTD_OK;
+}
+
 #ifdef BTD_PHASE_PROF
 int btd_debug_phase_cycles(unsigned long long* out16, int reset) {
   cudaDeviceSynchronize();

@@ -784,6 +784,16 @@ __global__ void assemble_schur_diag_kernel(const double* diag, const int* seps, 
   }
 }
 
+// Upper triangle of every n x n block := its lower triangle (debug export of Schur diagonals).
+__global__ void mirror_lower_kernel(double* blocks, long long P, int n) {
+  const size_t bs = (size_t)n * n, total = (size_t)P * bs;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = e / bs;
+    const int i = (int)(e % bs), r = i / n, c = i % n;
+    if (c > r) blocks[e] = blocks[b * bs + (size_t)c * n + r];
+  }
+}
+
 __global__ void fill_separators_kernel(int* seps, int P, int N, int step) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < P) seps[k] = (k == P - 1) ? N - 1 : k * step;

@@ -236,7 +236,7 @@ def recursive_factorize(matrix: BlockTridiagonalMatrix, config: RecursionConfig 
         return _factorize_on(matrix, config, s, profile)
 
 
-def _factorize_on(matrix, config, s, profile):
+def _factorize_on(matrix, config, s, profile, keep_scratch=False):
     import torch
     cfg = config or RecursionConfig()
     L = _native.lib()
@@ -273,6 +273,8 @@ def _factorize_on(matrix, config, s, profile):
         rc = L.btd_factorize_from_host(handle, hd, hs if N > 1 else None, diag.data_ptr(),
                                        sub.data_ptr() if N > 1 else None, persistent.data_ptr(),
                                        scratch.data_ptr(), ctypes.c_void_p(s.cuda_stream), 1, ctypes.byref(st))
+    if keep_scratch:
+        native.scratch = scratch
     del scratch
     if rc != _native.BTD_OK:
         _raise_status(st, rc)
@@ -374,6 +376,29 @@ def factor_kernel_times(matrix: BlockTridiagonalMatrix, config: RecursionConfig 
         l0.append(out[0])
     return {"factor_ms": statistics.median(f_ms), "solve_ms": statistics.median(s_ms),
             "level0_factor_ms": statistics.median(l0)}
+
+
+def level_schur(matrix: BlockTridiagonalMatrix, level: int, config: RecursionConfig | None = None):
+    """Debug view: the next-level Schur complement system (diag, sub) that level ``level`` of the
+    recursion hands to level ``level + 1`` -- what the reference's ``compute_schur`` + ``new_btd``
+    return (schur.py:156-193) -- as device tensors of the user's block size."""
+    import torch
+    with _on_stream(_matrix_device(matrix), None) as s:
+        h = _factorize_on(matrix, config, s, False, keep_scratch=True)
+        native = h._native
+        if not 0 <= level < len(h.levels):
+            raise ValueError(f"level {level} outside [0, {len(h.levels)})")
+        P = h.levels[level].num_separators
+        n = getattr(native, "padded", h.block_size)
+        diag = torch.empty((P, n, n), dtype=torch.float64, device=native.device)
+        sub = torch.empty((max(P - 1, 1), n, n), dtype=torch.float64, device=native.device)
+        st = _native.BtdStatus()
+        rc = _native.lib().btd_level_schur(native.handle, level, native.scratch.data_ptr(), diag.data_ptr(),
+                                           sub.data_ptr(), ctypes.c_void_p(s.cuda_stream), ctypes.byref(st))
+        if rc != _native.BTD_OK:
+            _raise_status(st, rc)
+        nu = h.block_size
+        return diag[:, :nu, :nu], sub[:max(P - 1, 0), :nu, :nu]
 
 
 def level_factor(hierarchy: FactorHierarchy, level: int):

@@ -128,10 +128,13 @@ def test_multi_column_equals_column_by_column():
         assert np.abs(xc[:, :, 0] - X[:, :, c]).max() <= 1e-13 * np.abs(X).max()
 
 
+@pytest.mark.slow
 @pytest.mark.parametrize("cfg", [(1024, 32, 1), (65536, 64, 1), (1048576, 8, 1), (4096, 256, 64)],
                          ids=["cfg1", "cfg2", "cfg3", "cfg4"])
-def test_baseline_configs_residual(cfg):
-    """Full BASELINE sizes: size-independent property (relative residual) + first rows vs oracle."""
+def test_baseline_configs_vs_oracle(cfg):
+    """Full BASELINE sizes (configs 1-4, seed 0): the device solution against the CPU oracle run on
+    the same inputs on the host cores (max|dX|/max|X| <= 1e-10) and the relative residual
+    (<= 1e-12, size-independent)."""
     N, n, d = cfg
     A, B = pkg.generate_spd_btd(N, n, d, seed=0)
     dA = pkg.BlockTridiagonalMatrix(torch.from_numpy(A.diag).cuda(), torch.from_numpy(A.sub).cuda())
@@ -140,6 +143,49 @@ def test_baseline_configs_residual(cfg):
     X = pkg.recursive_solve(h, dB)
     _, rres = pkg.residual_report(dA, X, dB)
     assert rres <= REL_RES, rres
+    levels = [lvl.num_blocks for lvl in h.levels] + [h.base.num_blocks]
+    x = X.blocks.cpu().numpy()
+    del dA, dB, X, h
+    torch.cuda.empty_cache()
+    hh = port.factorize(A.diag, A.sub)
+    assert levels == [N] + [len(r["seps"]) for r in hh["levels"]]
+    ref = port.solve(hh, B.blocks)
+    rel = np.abs(x - ref).max() / np.abs(ref).max()
+    assert rel <= REL_X, rel
+
+
+def test_level_schur_vs_reference_golden(golden):
+    """The next-level Schur complement system the GPU level kernels + assembly produce equals the
+    reference's own compute_schur + new_btd output (tests/golden: _factorize_level of the real
+    reference), <= 1e-12 x the block scale."""
+    i = 0
+    while f"schur{i}_meta" in golden:
+        N, n, seed, rho = (int(v) for v in golden[f"schur{i}_meta"])
+        A, _ = pkg.generate_spd_btd(N, n, 1, seed)
+        cfg = pkg.RecursionConfig(crossover=2, segment_length=rho)
+        diag, sub = pkg.level_schur(A, 0, cfg)
+        want_d, want_s = golden[f"schur{i}_diag"], golden[f"schur{i}_sub"]
+        scale = np.abs(want_d).max()
+        assert tuple(diag.shape) == want_d.shape and tuple(sub.shape) == want_s.shape
+        assert np.abs(diag.cpu().numpy() - want_d).max() <= 1e-12 * scale, i
+        assert np.abs(sub.cpu().numpy() - want_s).max() <= 1e-12 * scale, i
+        i += 1
+    assert i == 5
+
+
+@pytest.mark.parametrize("case", [(30000, 64, 8, 1), (30000, 64, 8, 2), (200000, 8, 8, 0), (3000, 128, 8, 0),
+                                  (5000, 32, 5, 1)], ids=str)
+def test_level_schur_vs_oracle(case):
+    """Every level's Schur system (levels 0..2) against the oracle's compute_schur at sizes beyond
+    the golden fixtures (n = 8 / 32 / 64 / 128 kernel families)."""
+    N, n, rho, level = case
+    A, _ = pkg.generate_spd_btd(N, n, 1, seed=level + 5)
+    cfg = pkg.RecursionConfig(crossover=64, segment_length=rho)
+    diag, sub = pkg.level_schur(A, level, cfg)
+    want_d, want_s = port.level_schur(A.diag, A.sub, level, 64, rho)
+    scale = np.abs(want_d).max()
+    assert np.abs(diag.cpu().numpy() - want_d).max() <= 1e-12 * scale
+    assert np.abs(sub.cpu().numpy() - want_s).max() <= 1e-12 * scale
 
 
 @pytest.mark.parametrize("case", [(20000, 16, 2, 2, 8, 3), (20000, 16, 2, 3, 8, 3), (30000, 64, 1, 4, 64, 8),
