@@ -14,10 +14,12 @@ e2e        = same metric through the public API with pinned HOST buffers (H2D of
              cover their lower triangle, the only part any kernel reads).
 roofline   = the dominant kernel (level-0 factor_level_kernel<64>), fp64 DMMA-bound, timed
              with CUDA events on the launching stream (C-ABI timing hook).
-Multi-GPU (torchrun, N > 1): the chain is sharded -- every rank owns a chunk of the
-configuration's size (weak scaling: N_global = N x chunk), eliminates its interiors locally and the
-reduced separator system is all-gathered over NCCL and solved redundantly; value = W_sub of the
-global chain / max-over-ranks time.
+Multi-GPU (N > 1; `--gpus N` self-launches N ranks through torch.distributed.run when WORLD_SIZE
+is unset): strong scaling of BASELINE config 5 (N = 2^20, n = 64, d = 4) -- the ONE seed-0
+instance is cut into G contiguous chunks at level-L separators, every rank
+generates exactly its slice of that instance (bit-identical, synthgen.generate_spd_btd_slice),
+eliminates its interiors locally, the reduced separator system is all-gathered over NCCL and
+solved redundantly; value = W_sub of the global chain / max-over-ranks time.
 """
 
 from __future__ import annotations
@@ -42,8 +44,13 @@ CONFIGS = {  # BASELINE.json configs
     "cfg2": (65536, 64, 1),
     "cfg3": (1048576, 8, 1),
     "cfg4": (4096, 256, 64),
+    "cfg5": (1048576, 64, 4),
 }
-CPU_SAMPLE = {"cfg1": (1024, 32, 1), "cfg2": (8192, 64, 1), "cfg3": (131072, 8, 1), "cfg4": (512, 256, 64)}
+DEFAULT_SINGLE, DEFAULT_MULTI = "cfg2", "cfg5"
+# CPU (reference-port) sample per config: the full instance where one factor+solve takes <~30 s on
+# the GPU hosts' cores (cfg1, cfg2: same config as the GPU arm), else a bounded prefix-sized sample
+CPU_SAMPLE = {"cfg1": (1024, 32, 1), "cfg2": (65536, 64, 1), "cfg3": (131072, 8, 1), "cfg4": (512, 256, 64),
+              "cfg5": (32768, 64, 4)}
 
 
 # ------------------------------------------------------------------------------------------
@@ -94,6 +101,39 @@ def q_min(N, n, d):
     return 8.0 * (3.0 * (2 * N - 1) * n * n + 2.0 * N * n * d)
 
 
+def packed_stride(n):
+    k = n >> 1
+    return 2 * (k + 1) * (k + 1) if n & 1 else 2 * k * (k + 1)
+
+
+def level0_bytes(N, n, rho=8):
+    """Algorithmic HBM bytes of one level-0 factor launch: read the interior diagonal blocks and
+    every sub block, write Linv (packed) of the interior rows, L_sub / the coupling copies, and
+    S_L, S_R, S_sub per segment (btd_factor.cuh / btd_small.cuh)."""
+    levels, _ = plan_levels(N, rho=rho)
+    N0, lens = levels[0]
+    K = len(lens)
+    interior = int(lens.sum())
+    nn = n * n
+    return 8.0 * (interior * nn + (N0 - 1) * nn + interior * packed_stride(n) + (N0 - 1) * nn + 3 * K * nn)
+
+
+def bound_of(N, n, d, peak_tflops, hbm_gbs):
+    """'tensor' (fp64 pipe) or 'hbm': whichever roofline term is larger."""
+    f, s_, _ = w_sub(N, n, d)
+    return "tensor" if (f + s_) / (peak_tflops * 1e12) >= q_min(N, n, d) / (hbm_gbs * 1e9) else "hbm"
+
+
+def measured_peaks():
+    """(fp64 DMMA TFLOP/s, HBM GB/s, source note)."""
+    fp = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak_r01.json")))["dmma_m8n8k4_tflops"]
+    hbm, src = 6556.2, "fallback 6556.2 GB/s"
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        hbm, src = float(json.load(open(mp))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    return fp, hbm, src
+
+
 # ------------------------------------------------------------------------------------------
 # clocks sampling (B200_PROFILING.md clocks line)
 # ------------------------------------------------------------------------------------------
@@ -139,47 +179,72 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------
 # CPU baseline (oracle port of the reference algorithm, timed on the host cores)
 # ------------------------------------------------------------------------------------------
-def cpu_baseline(cfg_name, runs=1):
-    from oracle import blocktri_port as port
+def _cpu_instance(cfg_name):
     from paper_2509_03015_b200.synthgen import generate_spd_btd
     N, n, d = CPU_SAMPLE[cfg_name]
     A, B = generate_spd_btd(N, n, d, seed=0)
-    t = []
-    for _ in range(runs):
-        t0 = time.perf_counter()
-        h = port.factorize(A.diag, A.sub)
-        port.solve(h, B.blocks)
-        t.append(time.perf_counter() - t0)
+    return (N, n, d), A, B
+
+
+def _cpu_step(A, B):
+    from oracle import blocktri_port as port
+    t0 = time.perf_counter()
+    h = port.factorize(A.diag, A.sub)
+    port.solve(h, B.blocks)
+    return time.perf_counter() - t0
+
+
+def _cpu_sample_note(cfg_name, runs, sec):
+    from oracle import blocktri_port as port
+    N, n, d = CPU_SAMPLE[cfg_name]
+    same = CPU_SAMPLE[cfg_name] == CONFIGS[cfg_name]
+    what = "the full instance (same config as the GPU arm)" if same else f"a bounded sample N={N}"
+    return (f"{what}: N={N} n={n} d={d}, reference generator seed 0, {runs} run(s), median {sec * 1e3:.0f} ms "
+            f"factor+solve; oracle/blocktri_port.py F-form restatement of the reference, pool={port._threads()} "
+            f"threads, BLAS threads default, host cpus={os.cpu_count()}")
+
+
+def cpu_baseline(cfg_name, runs=1):
+    from oracle import blocktri_port as port
+    (N, n, d), A, B = _cpu_instance(cfg_name)
+    sec = statistics.median([_cpu_step(A, B) for _ in range(runs)])
     f, s, _ = w_sub(N, n, d)
-    sec = statistics.median(t)
     return {"value": (f + s) / sec / 1e9, "unit": "GFLOP/s", "cores": port._threads(), "kind": "port",
-            "sample": f"N={N} n={n} d={d} (same generator/seed, {runs} run(s), median {sec * 1e3:.0f} ms "
-                      f"factor+solve; oracle/blocktri_port.py F-form restatement, pool={port._threads()} threads, "
-                      f"BLAS threads default, host cpus={os.cpu_count()})"}
+            "same_config": CPU_SAMPLE[cfg_name] == CONFIGS[cfg_name], "sample": _cpu_sample_note(cfg_name, runs, sec)}
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm (oracle port, pinned to the real reference's
+    outputs) on the host cores, rank 0 only; each step is one factor+solve of the CPU sample."""
     if rank != 0:
         return
+    from oracle import blocktri_port as port
     cfg = args.config
     N, n, d = CONFIGS[cfg]
-    vals = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_baseline(cfg, runs=1)
-        if i >= args.warmup:
-            vals.append(r["value"])
-    v = statistics.median(vals)
-    Ns, ns, ds = CPU_SAMPLE[cfg]
+    (Ns, ns, ds), A, B = _cpu_instance(cfg)
+    for _ in range(min(args.warmup, 1)):  # a CPU step needs no graph/allocator warm-up beyond one
+        _cpu_step(A, B)
+    budget, times = 300.0, []  # bound the arm to ~5 minutes of timed steps
+    t_start = time.perf_counter()
+    while len(times) < args.steps:
+        times.append(_cpu_step(A, B))
+        if time.perf_counter() - t_start + times[-1] > budget:
+            break
+    sec = statistics.median(times)
     fs, ss, _ = w_sub(Ns, ns, ds)
+    v = (fs + ss) / sec / 1e9
+    same = (Ns, ns, ds) == (N, n, d)
     line = {
         "impl": "reference", "metric": "fp64 factor+solve GFLOP/s (W_sub), block-tridiagonal SPD N x n",
-        "value": round(v, 4), "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round((fs + ss) / (v * 1e9) * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "value": round(v, 4), "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": len(times),
+        "steps_requested": args.steps, "warmup": min(args.warmup, 1),
+        "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generate_spd_btd, seed 0)",
-        "config": {"workload": f"{cfg}: N={N} n={n} d={d} (CPU step = bounded sample N={Ns})",
+        "config": {"workload": f"{cfg}: N={N} n={n} d={d}" + ("" if same else f" (CPU step = bounded sample N={Ns})"),
                    "crossover": 64, "segment_length": 8},
-        "cpu_baseline": {"value": round(v, 4), "unit": "GFLOP/s", "cores": r["cores"], "kind": "port",
-                         "sample": r["sample"]},
+        "same_config": same,
+        "cpu_baseline": {"value": round(v, 4), "unit": "GFLOP/s", "cores": port._threads(), "kind": "port",
+                         "sample": _cpu_sample_note(cfg, len(times), sec)},
         "e2e": {"value": round(v, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -210,7 +275,7 @@ def run_ours(args, rank, world):
     hd = torch.empty((N, n, n), dtype=torch.float64).pin_memory()
     hs = torch.empty((N - 1, n, n), dtype=torch.float64).pin_memory()
     hb = torch.empty((N, n, d), dtype=torch.float64).pin_memory()
-    pkg.generate_spd_btd(N, n, d, seed=rank, out=(hd.numpy(), hs.numpy(), hb.numpy()))
+    pkg.generate_spd_btd(N, n, d, seed=0, out=(hd.numpy(), hs.numpy(), hb.numpy()))
     dA = pkg.BlockTridiagonalMatrix(hd.to(dev), hs.to(dev))
     dB = pkg.BlockRhs(hb.to(dev))
     torch.cuda.synchronize()
@@ -220,7 +285,9 @@ def run_ours(args, rank, world):
         h = pkg.recursive_factorize(dA)
         return h, pkg.recursive_solve(h, dB)
 
+    h = X = None
     for _ in range(max(args.warmup, 3)):
+        h = X = None  # release the previous factor first (cfg5's hierarchy is ~55 GB)
         h, X = step()
     torch.cuda.synchronize()
     _, rres = pkg.residual_report(dA, X, dB)
@@ -239,6 +306,7 @@ def run_ours(args, rank, world):
     launches0 = _native.lib().btd_launch_count()
     ev[0].record(stream)
     for _ in range(args.steps):
+        h = X = None
         h, X = step()
     ev[1].record(stream)
     torch.cuda.synchronize()
@@ -251,20 +319,25 @@ def run_ours(args, rank, world):
         dist.barrier()
 
     # per-launch timing of the dominant kernel (level-0 factor) through the C-ABI timing hook
-    L = _native.lib()
+    h = X = None
     kt = pkg.schur.factor_kernel_times(dA, repeats=3)
     clocks = sampler.stop(dev.index) if sampler else None
+    del dA, dB
+    torch.cuda.empty_cache()  # the host-input path below allocates its own device arenas
 
     # end to end: pinned host buffers -> public API -> host solution
     hA = pkg.BlockTridiagonalMatrix(hd, hs)
     hB = pkg.BlockRhs(hb)
     for _ in range(2):  # untimed warm-up of the host-buffer path (workspaces, pinned staging, graphs)
-        pkg.recursive_solve(pkg.recursive_factorize(hA), hB)
+        Xh = None
+        Xh = pkg.recursive_solve(pkg.recursive_factorize(hA), hB)
     torch.cuda.synchronize()
+    hh = Xh = None
     # every step ends with the solution on the host (a host sync), so each step is timed on its own;
     # the median over the K steps is reported (PCIe throughput of a fresh box fluctuates step to step)
     e2e_each = []
     for _ in range(args.steps):
+        hh = Xh = None
         t0 = time.perf_counter()
         hh = pkg.recursive_factorize(hA)
         Xh = pkg.recursive_solve(hh, hB)
@@ -283,32 +356,40 @@ def run_ours(args, rank, world):
     e2e = (f + s) / (e2e_ms * 1e-3) / 1e9 * world
     if rank != 0:
         return
-    peaks = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak_r01.json")))
-    peak = peaks["dmma_m8n8k4_tflops"]
+    peak_fp, hbm, hbm_src = measured_peaks()
+    bound = bound_of(N, n, d, peak_fp, hbm)
     l0_ms = kt["level0_factor_ms"]
-    achieved = f0 / (l0_ms * 1e-3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"ncu_{cfg}_factor_l0.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+    if bound == "tensor":
+        achieved, peak, unit = f0 / (l0_ms * 1e-3) / 1e12, peak_fp, "TFLOP/s"
+        peak_source = "profiles/fp64_peak_r01.json (measured fp64 DMMA; MEASURED_PEAKS.json has no fp64)"
+        whole = (f + s) / (ms * 1e-3) / 1e12 / peak_fp
+        algo = {"algorithmic_flops": f0}
+    else:
+        b0 = level0_bytes(N, n)
+        achieved, peak, unit = b0 / (l0_ms * 1e-3) / 1e9, hbm, "GB/s"
+        peak_source = hbm_src
+        whole = q_min(N, n, d) / (ms * 1e-3) / 1e9 / hbm
+        algo = {"algorithmic_bytes": b0}
     cpu = cpu_baseline(cfg) if world == 1 and not args.no_cpu else None
     line = {
         "metric": "fp64 factor+solve GFLOP/s (W_sub), block-tridiagonal SPD N x n",
         "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference generate_spd_btd stream, seed=rank; inputs 4.3 GB > L2, no flush)",
+        "data": "synthetic (reference generate_spd_btd stream, seed 0; inputs > L2, no flush)",
         "config": {"workload": f"{cfg}: N={N} n={n} d={d}", "crossover": 64, "segment_length": 8,
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "l2": "inputs larger than L2"},
+                   "parallelism": "single GPU", "l2": "inputs larger than L2"},
         "factor_ms": round(kt["factor_ms"], 4), "solve_ms": round(kt["solve_ms"], 4),
         "rel_residual": rres, "w_sub_gflop": round((f + s) / 1e9, 3), "q_min_gb": round(q_min(N, n, d) / 1e9, 3),
-        "roofline": {"bound": "tensor", "kernel": kernel_name(n),
-                     "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
+        "roofline": {"bound": bound, "kernel": kernel_name(n),
+                     "achieved": round(achieved, 3), "peak": peak, "unit": unit,
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "peak_source": "profiles/fp64_peak_r01.json (measured fp64 DMMA; MEASURED_PEAKS.json has no fp64)",
-                     "launch_ms": round(l0_ms, 4), "algorithmic_flops": f0,
-                     "whole_step_frac": round((f + s) / (ms * 1e-3) / 1e12 / peak, 4)},
+                     "peak_source": peak_source, "launch_ms": round(l0_ms, 4), **algo,
+                     "whole_step_frac": round(whole, 4)},
         "e2e": {"value": round(e2e, 3), "unit": "GFLOP/s", "ms_per_step": round(e2e_ms, 3),
                 "ms_per_step_mean": round(e2e_mean, 3), "timing": f"median of {args.steps} host-timed steps",
                 "h2d_bytes_per_step": int(diag_h2d_bytes(N, n) + hs.numel() * 8 + hb.numel() * 8),
@@ -322,31 +403,50 @@ def run_ours(args, rank, world):
 
 
 # ------------------------------------------------------------------------------------------
-# N > 1: the sharded chain, weak scaling -- every rank owns a chunk of the
-# configuration's size, the reduced separator system is all-gathered over NCCL
+# N > 1: strong scaling of config 5 over the sharded chain -- every rank slices
+# its chunk of the ONE global seed-0 instance; the reduced separator system is all-gathered
 # ------------------------------------------------------------------------------------------
+def sharded_residual(plan, rank, dd, ds, db, x, dist):
+    """Global max-column ||b - A x|| / ||b|| of the distributed solution.  Each rank owns the rows
+    (a_g, b_g] of its chunk (rank 0 also row 0); the coupling term A_{b+1,b}^T x_{b+1} of a chunk's
+    last row lives on the right neighbour and is all-gathered (one n x d panel per rank)."""
+    import torch
+    from paper_2509_03015_b200 import report
+    y = report.btd_matmul(sh_matrix(dd, ds), sh_rhs(x)).blocks
+    G = plan.G
+    part = (ds[0].transpose(0, 1) @ x[1]) if rank > 0 else torch.zeros_like(x[0])
+    parts = [torch.empty_like(part) for _ in range(G)]
+    dist.all_gather(parts, part.contiguous())
+    lo = 0 if rank == 0 else 1
+    r = db[lo:] - y[lo:]
+    if rank < G - 1:
+        r[-1] -= parts[rank + 1]
+    d = x.shape[2]
+    sums = torch.stack([(r.reshape(-1, d) ** 2).sum(0), (db[lo:].reshape(-1, d) ** 2).sum(0)])
+    dist.all_reduce(sums)
+    return float((sums[0] / sums[1]).sqrt().max())
+
+
 def run_sharded(args, rank, world):
     import torch
     import torch.distributed as dist
+    from paper_2509_03015_b200 import _native
     from paper_2509_03015_b200 import sharded as sh
-    from paper_2509_03015_b200.synthgen import generate_spd_btd
+    from paper_2509_03015_b200.synthgen import generate_spd_btd_slice
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     cfg = args.config
-    N1, n, d = CONFIGS[cfg]
-    plan = sh.shard_plan(N1 * world, world)
+    N, n, d = CONFIGS[cfg]
+    plan = sh.shard_plan(N, world)
     a, b = plan.chunk(rank)
     Nc = b - a + 1
-    # synthetic chunk: the reference generator's stream with seed = rank; the shared boundary
-    # block is owned by the left rank (diagonal shifted by n so it also dominates the right
-    # neighbour's coupling, |A_{b+1,b}| row sums <= n), the right rank passes zeros for it
+    # this rank's slice of the global instance (bit-identical to the unsharded generator); the
+    # shared boundary block / rhs panel is owned by the left rank (sharded.chunk_inputs rule)
     hd = torch.empty((Nc, n, n), dtype=torch.float64).pin_memory()
     hs = torch.empty((Nc - 1, n, n), dtype=torch.float64).pin_memory()
     hb = torch.empty((Nc, n, d), dtype=torch.float64).pin_memory()
-    generate_spd_btd(Nc, n, d, seed=rank, out=(hd.numpy(), hs.numpy(), hb.numpy()))
-    if rank < world - 1:
-        hd[-1] += n * torch.eye(n, dtype=torch.float64)
+    generate_spd_btd_slice(N, n, d, 0, a, b, out=(hd.numpy(), hs.numpy(), hb.numpy()))
     if rank > 0:
         hd[0] = 0.0
         hb[0] = 0.0
@@ -363,21 +463,13 @@ def run_sharded(args, rank, world):
     for _ in range(max(args.warmup, 3)):
         x = step(dd, ds, db)
     torch.cuda.synchronize()
-    # residual of this rank's interior rows (rows 1..Nc-2 only involve the chunk's own blocks)
-    from paper_2509_03015_b200 import report
-    y = report.btd_matmul(sh_matrix(dd, ds), sh_rhs(x)).blocks
-    r = (db[1:-1] - y[1:-1]).reshape(-1, d)
-    rres = float((torch.linalg.vector_norm(r, dim=0) / torch.linalg.vector_norm(db[1:-1].reshape(-1, d), dim=0)).max())
-    t = torch.tensor([rres], device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    rres = float(t)
+    rres = sharded_residual(plan, rank, dd, ds, db, x, dist)
 
     sampler = ClockSampler() if rank == 0 else None
     if sampler:
         sampler.start()
         time.sleep(0.3)
     stream = torch.cuda.current_stream(dev)
-    from paper_2509_03015_b200 import _native
     launches0 = _native.lib().btd_launch_count()
     dist.barrier()
     torch.cuda.synchronize()
@@ -409,25 +501,28 @@ def run_sharded(args, rank, world):
     t = torch.tensor([e2e_ms], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t)
-    f, s_, _ = w_sub(plan.N, n, d)
+    h2d = torch.tensor([(hd.numel() + hs.numel() + hb.numel()) * 8, hb.numel() * 8], device=dev, dtype=torch.float64)
+    dist.all_reduce(h2d)
+    f, s_, _ = w_sub(N, n, d)
     if rank != 0:
         return
     line = {
         "metric": "fp64 factor+solve GFLOP/s (W_sub), block-tridiagonal SPD N x n",
         "value": round((f + s_) / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference generate_spd_btd stream per chunk, seed=rank; inputs > L2, no flush)",
-        "config": {"workload": f"{cfg} chunk per GPU, sharded chain: N={plan.N} (={world} x ~{N1}) n={n} d={d}",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (the reference generator's seed-0 instance, each rank its own slice; inputs > L2, no flush)",
+        "config": {"workload": f"{cfg}: N={N} n={n} d={d}, one chain sharded over {world} GPUs",
                    "crossover": 64, "segment_length": 8, "parallelism": f"chain sharded x{world}",
-                   "local_levels": plan.L, "reduced_blocks": plan.reduced_N, "l2": "inputs larger than L2"},
-        "rel_residual_interior": rres, "w_sub_gflop": round((f + s_) / 1e9, 3),
+                   "local_levels": plan.L, "reduced_blocks": plan.reduced_N, "cuts": plan.cuts,
+                   "l2": "inputs larger than L2"},
+        "rel_residual": rres, "w_sub_gflop": round((f + s_) / 1e9, 3),
         "e2e": {"value": round((f + s_) / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s", "ms_per_step": round(e2e_ms, 3),
-                "h2d_bytes_per_step": int((hd.numel() + hs.numel() + hb.numel()) * 8) * world,
-                "d2h_bytes_per_step": int(hb.numel() * 8) * world},
+                "h2d_bytes_per_step": int(h2d[0]), "d2h_bytes_per_step": int(h2d[1])},
         "gpu_launches": int(launches),
         "clocks": clocks,
-        "collective": "torch.distributed all_gather of the reduced separator system (factor) and rhs (solve)",
+        "collective": f"torch.distributed ({dist.get_backend()}) all_gather of the reduced separator system "
+                      "(factor) and of the reduced rhs (solve)",
     }
     print(json.dumps(line), flush=True)
 
@@ -442,30 +537,50 @@ def sh_rhs(x):
     return BlockRhs(x)
 
 
+def self_launch(args):
+    """`--gpus N` with N > 1 and no torchrun environment: re-run this script as N ranks."""
+    import socket
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help=f"default: {DEFAULT_SINGLE} on one GPU, {DEFAULT_MULTI} (strong scaling) on N > 1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    if world > 1 and args.impl == "ours":
+    if args.config is None:
+        args.config = DEFAULT_SINGLE if world == 1 else DEFAULT_MULTI
+    dist_on = world > 1 and args.impl == "ours"
+    if dist_on:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
-        # BTD_BENCH_GLOO=1: host-staged gloo collectives (lets N ranks share one GPU for a dry run)
-        dist.init_process_group("gloo" if os.environ.get("BTD_BENCH_GLOO") == "1" else "nccl")
+        ndev = torch.cuda.device_count()
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % ndev)
+        # more ranks than GPUs (a dry run of N ranks on one device): NCCL refuses duplicate GPUs, so
+        # the collectives are host-staged over gloo; BTD_BENCH_GLOO=1 forces that
+        gloo = os.environ.get("BTD_BENCH_GLOO") == "1" or world > ndev
+        dist.init_process_group("gloo" if gloo else "nccl")
     if args.impl == "reference":
         run_reference(args, rank, world)
     elif world > 1:
         run_sharded(args, rank, world)
     else:
         run_ours(args, rank, world)
-    if world > 1 and args.impl == "ours":
+    if dist_on:
         import torch.distributed as dist
         dist.destroy_process_group()
 

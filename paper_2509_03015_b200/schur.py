@@ -359,7 +359,9 @@ def factor_kernel_times(matrix: BlockTridiagonalMatrix, config: RecursionConfig 
     f_ms, s_ms, l0 = [], [], []
     rhs = BlockRhs(torch.ones((matrix.num_blocks, matrix.block_size, 1), dtype=torch.float64,
                               device=matrix.diag.device))
+    h = None
     for _ in range(repeats):
+        h = None  # release the previous factor before the next one is allocated
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         e[0].record()
         h = recursive_factorize(matrix, config, profile=True)

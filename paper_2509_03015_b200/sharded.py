@@ -344,12 +344,30 @@ class ShardedSolver:
 
 def run_sharded_local(plan: ShardPlan, engine, diag, sub, rhs, config=None):
     """All G ranks of the sharded algorithm played sequentially in one process (single-GPU check
-    of the per-rank kernels and the assembly; the collective is the identity)."""
+    of the per-rank kernels and the assembly; the collective is the identity).
+
+    Torch inputs are not copied chunk by chunk (a config-5 matrix is 64 GiB): chunk g > 0 sees its
+    shared boundary block zeroed only while its factor is enqueued, and the block is restored
+    right after on the same stream (stream order keeps both neighbours' reads correct)."""
     cfg = plan.config(config)
     states, rds, rss, rhs_c = [], [], [], []
+    is_torch = type(diag).__module__.startswith("torch")
     for g in range(plan.G):
-        d, s, r = chunk_inputs(plan, g, diag, sub, rhs)
-        st, rd, rs = engine.factor_partial(d, s, plan.L, cfg)
+        if is_torch:
+            a, b = plan.chunk(g)
+            d, s = diag[a:b + 1], sub[a:b]
+            r = rhs[a:b + 1].clone()
+            saved = None
+            if g > 0:
+                saved = d[0].clone()
+                d[0].zero_()
+                r[0] = 0.0
+            st, rd, rs = engine.factor_partial(d, s, plan.L, cfg)
+            if saved is not None:
+                d[0].copy_(saved)
+        else:
+            d, s, r = chunk_inputs(plan, g, diag, sub, rhs)
+            st, rd, rs = engine.factor_partial(d, s, plan.L, cfg)
         if rd.shape[0] != plan.reduced_sizes[g]:
             raise AssertionError(f"chunk {g}: reduced size {rd.shape[0]} != planned {plan.reduced_sizes[g]}")
         states.append(st)
