@@ -46,6 +46,7 @@ extern "C" {
 #define BTD_ERR_UNSUPPORTED 5           /* block size outside the compiled kernel set */
 #define BTD_ERR_CUDA 6                  /* CUDA runtime error (message carries cudaGetErrorString) */
 #define BTD_ERR_NOT_FACTORED 7          /* reference ValueError("batch must be factorized ...") */
+#define BTD_ERR_SINGULAR_DIAGONAL 8     /* reference SingularDiagonal(row, member) (errors.py:71-78) */
 
 /* RecursionConfig (schur.py:43-64). All knobs must be >= 1. */
 typedef struct btd_config {
@@ -195,6 +196,34 @@ long long btd_launch_count(void);
 int btd_set_graphs(int32_t enable);
 /* Process-wide count of factor / solve calls served by replaying a cached graph. */
 long long btd_graph_replays(void);
+
+/* ---- The reference's accelerator seam (bt/kernels.py:164-338) ----
+ * Batched dense kernels over `count` same-shaped members of ANY element strides (member, row,
+ * column) -- the reference solves through transposed views (block_cholesky.py:32).  All pointers are
+ * device pointers; launches are asynchronous on `stream`.  Failures accumulate in a device error
+ * word (btd_seam_error_bytes() bytes, reset by btd_seam_error_init) exactly as the reference's
+ * chunked batch reports them: NotPositiveDefinite = earliest `block_coord`, then lowest member,
+ * 1-based pivot; SingularDiagonal = lowest (member, row).  btd_seam_error_read synchronizes `stream`
+ * and returns BTD_OK / BTD_ERR_NOT_POSITIVE_DEFINITE (pivot, member, block) /
+ * BTD_ERR_SINGULAR_DIAGONAL (pivot = 1-based row, member). */
+size_t btd_seam_error_bytes(void);
+int btd_seam_error_init(void* err, void* stream);
+int btd_seam_error_read(const void* err, void* stream, btd_status* st);
+/* chol_factor_batch (kernels.py:164-181): member = L L^T in place, strict upper triangle zeroed.
+ * block_coord = the block step reported with a failure (_chol_step, block_cholesky.py:40-42). */
+int btd_chol_batch(double* blocks, const int64_t strides[3], int64_t count, int64_t n, int64_t block_coord, void* err,
+                   void* stream, btd_status* st);
+/* trsm_lower_batch (kernels.py:215-259): panels (count, n, cols) <- L^{-1} P (trans = 0) or
+ * L^{-T} P (trans = 1), L = lower triangle of factors (count, n, n).  A zero diagonal anywhere is
+ * reported and no panel is modified. */
+int btd_trsm_batch(const double* factors, const int64_t fstrides[3], double* panels, const int64_t pstrides[3],
+                   int64_t count, int64_t n, int64_t cols, int32_t trans, void* err, void* stream, btd_status* st);
+/* gemm_acc_batch (kernels.py:270-310): out (count, m, p) <- alpha op(a) op(b) + beta out, op(a) m x q,
+ * op(b) q x p; alpha == 0 skips the product, beta == 0 ignores out's contents.  out must not alias
+ * a or b.  At most 65535 members per call. */
+int btd_gemm_batch(double* out, const int64_t ostrides[3], const double* a, const int64_t astrides[3], const double* b,
+                   const int64_t bstrides[3], int64_t count, int64_t m, int64_t q, int64_t p, int32_t trans_a,
+                   int32_t trans_b, double alpha, double beta, void* stream, btd_status* st);
 
 #ifdef __cplusplus
 }

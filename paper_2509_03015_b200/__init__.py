@@ -16,6 +16,10 @@ from .report import (SWEEPS, BenchRow, bench_sweep, btd_matmul, device_bytes, fo
                      residual_report, time_call)
 from .kalman import StateSpaceModel, build_normal_equations, generate_rotation_model
 from .btdfile import read_btd, write_btd
+from .core import SegmentBatch
+from .kernels import (KernelBatchView, batched, chol_factor, chol_factor_batch, gemm_acc, gemm_acc_batch,
+                      max_batch_threads, set_batch_threads, trsm_lower, trsm_lower_batch)
+from .block_cholesky import factorize_btd_batch, serial_factorize, serial_solve, solve_btd_batch
 
 __version__ = "0.1.0"
 
@@ -27,5 +31,8 @@ __all__ = [
     "NotPositiveDefinite", "PartitionPlan", "RecursionConfig", "SingularDiagonal", "btd_matmul",
     "check_conformal", "generate_spd_btd", "level_factor", "level_schur", "new_btd", "new_rhs", "plan_partition",
     "recursive_factorize", "recursive_solve", "residual_report",
+    "SegmentBatch", "KernelBatchView", "batched", "chol_factor", "chol_factor_batch", "gemm_acc", "gemm_acc_batch",
+    "max_batch_threads", "set_batch_threads", "trsm_lower", "trsm_lower_batch", "factorize_btd_batch",
+    "serial_factorize", "serial_solve", "solve_btd_batch",
     "SWEEPS", "BenchRow", "bench_sweep", "device_bytes", "format_table", "parse_sweep", "time_call",
 ]

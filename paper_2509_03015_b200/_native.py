@@ -30,6 +30,7 @@ BTD_ERR_INVALID_ARGUMENT = 4
 BTD_ERR_UNSUPPORTED = 5
 BTD_ERR_CUDA = 6
 BTD_ERR_NOT_FACTORED = 7
+BTD_ERR_SINGULAR_DIAGONAL = 8
 
 #: every symbol include/blocktri_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED_SYMBOLS = (
@@ -39,6 +40,8 @@ EXPORTED_SYMBOLS = (
     "btd_create_partial", "btd_reduced_size", "btd_factorize_partial", "btd_solve_down", "btd_solve_up", "btd_launch_count",
     "btd_matmul", "btd_residual_workspace", "btd_residual_norms", "btd_factorize_from_host",
     "btd_kalman_workspace", "btd_kalman_normal_equations", "btd_set_graphs", "btd_graph_replays",
+    "btd_seam_error_bytes", "btd_seam_error_init", "btd_seam_error_read", "btd_chol_batch", "btd_trsm_batch",
+    "btd_gemm_batch",
 )
 
 
@@ -119,9 +122,18 @@ def lib() -> ctypes.CDLL:
         L.btd_matmul.argtypes = [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, P(BtdStatus)]
         L.btd_residual_workspace.argtypes = [c_i64, c_i64, c_i64, P(c_sz)]
         L.btd_residual_norms.argtypes = [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, P(BtdStatus)]
+        I64x3 = P(c_i64)
+        L.btd_seam_error_bytes.argtypes = []
+        L.btd_seam_error_bytes.restype = c_sz
+        L.btd_seam_error_init.argtypes = [c_vp, c_vp]
+        L.btd_seam_error_read.argtypes = [c_vp, c_vp, P(BtdStatus)]
+        L.btd_chol_batch.argtypes = [c_vp, I64x3, c_i64, c_i64, c_i64, c_vp, c_vp, P(BtdStatus)]
+        L.btd_trsm_batch.argtypes = [c_vp, I64x3, c_vp, I64x3, c_i64, c_i64, c_i64, c_i32, c_vp, c_vp, P(BtdStatus)]
+        L.btd_gemm_batch.argtypes = [c_vp, I64x3, c_vp, I64x3, c_vp, I64x3, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32,
+                                     ctypes.c_double, ctypes.c_double, c_vp, P(BtdStatus)]
         for name in EXPORTED_SYMBOLS:
             if name not in ("btd_version", "btd_default_config", "btd_destroy", "btd_launch_count",
-                            "btd_graph_replays"):
+                            "btd_graph_replays", "btd_seam_error_bytes"):
                 getattr(L, name).restype = ctypes.c_int
         L.btd_launch_count.restype = ctypes.c_longlong
         L.btd_graph_replays.restype = ctypes.c_longlong

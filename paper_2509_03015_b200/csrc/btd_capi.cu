@@ -24,6 +24,7 @@
 #include "btd_spmv.cuh"
 #include "btd_small.cuh"
 #include "btd_kalman.cuh"
+#include "btd_seam.cuh"
 
 namespace {
 
@@ -1964,6 +1965,113 @@ int btd_kalman_normal_equations(int64_t horizon, int64_t n, int64_t m, const dou
     return BTD_ERR_NOT_POSITIVE_DEFINITE;
   }
   return BTD_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Accelerator seam (btd_seam.cuh): chol_factor_batch / trsm_lower_batch / gemm_acc_batch,
+// bt/kernels.py:164-338.
+// ---------------------------------------------------------------------------------------------
+static btd::Strides to_strides(const int64_t* s) { return btd::Strides{(long long)s[0], (long long)s[1], (long long)s[2]}; }
+
+size_t btd_seam_error_bytes(void) { return sizeof(btd::SeamErr); }
+
+int btd_seam_error_init(void* err, void* stream) {
+  if (!err) return BTD_ERR_INVALID_ARGUMENT;
+  btd::seam_err_init_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((btd::SeamErr*)err);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError() == cudaSuccess ? BTD_OK : BTD_ERR_CUDA;
+}
+
+int btd_seam_error_read(const void* err, void* stream, btd_status* st) {
+  clear_status(st);
+  btd::SeamErr h;
+  cudaError_t e = cudaMemcpyAsync(&h, err, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(st, e, "btd_seam_error_read");
+  if (h.sing != btd::kNoErr) {
+    const long long member = (long long)(h.sing >> 24);
+    const int row = (int)(h.sing & 0xffffff);
+    set_status(st, BTD_ERR_SINGULAR_DIAGONAL, "triangular factor has zero diagonal at row %d, member %lld", row + 1,
+               member);
+    st->pivot = row + 1;
+    st->member = member;
+    return BTD_ERR_SINGULAR_DIAGONAL;
+  }
+  if (h.npd != btd::kNoErr) {
+    btd::DevErr de{h.npd, 0, 0};
+    decode_error(de, st);
+    st->level = -1;
+    return BTD_ERR_NOT_POSITIVE_DEFINITE;
+  }
+  return BTD_OK;
+}
+
+int btd_chol_batch(double* blocks, const int64_t strides[3], int64_t count, int64_t n, int64_t block_coord, void* err,
+                   void* stream, btd_status* st) {
+  clear_status(st);
+  if (!err || !strides || count < 0 || n < 1 || n > 0xffff || block_coord < 0 || block_coord > btd::kMaxBlockCoord ||
+      count > btd::kMaxMemberCoord || (count > 0 && !blocks)) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_chol_batch: bad arguments");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  if (count == 0) return BTD_OK;
+  const size_t smem = n <= btd::kSeamSmemMaxN ? (size_t)n * n * sizeof(double) : 0;
+  cudaError_t e = ensure_smem((const void*)btd::seam_chol_kernel, smem);
+  if (e != cudaSuccess) return cuda_fail(st, e, "btd_chol_batch(attr)");
+  btd::seam_chol_kernel<<<(unsigned)count, btd::kSeamThreads, smem, (cudaStream_t)stream>>>(
+      blocks, to_strides(strides), (int)n, (long long)block_coord, (btd::SeamErr*)err);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? BTD_OK : cuda_fail(st, e, "btd_chol_batch");
+}
+
+int btd_trsm_batch(const double* factors, const int64_t fstrides[3], double* panels, const int64_t pstrides[3],
+                   int64_t count, int64_t n, int64_t cols, int32_t trans, void* err, void* stream, btd_status* st) {
+  clear_status(st);
+  if (!err || !fstrides || !pstrides || count < 0 || n < 1 || cols < 0 || count > (1ll << 39) || n > (1 << 24) ||
+      (count > 0 && (!factors || !panels))) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_trsm_batch: bad arguments");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  if (count == 0) return BTD_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  btd::seam_diag_check_kernel<<<(unsigned)count, 128, 0, s>>>(factors, to_strides(fstrides), (int)n, count,
+                                                              (btd::SeamErr*)err);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (cols > 0) {
+    const size_t smem = n <= btd::kSeamSmemMaxN ? (size_t)n * n * sizeof(double) : 0;
+    cudaError_t e = ensure_smem((const void*)btd::seam_trsm_kernel, smem);
+    if (e != cudaSuccess) return cuda_fail(st, e, "btd_trsm_batch(attr)");
+    dim3 grid((unsigned)count, (unsigned)((cols + btd::kSeamThreads - 1) / btd::kSeamThreads));
+    btd::seam_trsm_kernel<<<grid, btd::kSeamThreads, smem, s>>>(factors, to_strides(fstrides), panels,
+                                                                 to_strides(pstrides), (int)n, (int)cols, trans,
+                                                                 (const btd::SeamErr*)err);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BTD_OK : cuda_fail(st, e, "btd_trsm_batch");
+}
+
+int btd_gemm_batch(double* out, const int64_t ostrides[3], const double* a, const int64_t astrides[3], const double* b,
+                   const int64_t bstrides[3], int64_t count, int64_t m, int64_t q, int64_t p, int32_t trans_a,
+                   int32_t trans_b, double alpha, double beta, void* stream, btd_status* st) {
+  clear_status(st);
+  if (!ostrides || !astrides || !bstrides || count < 0 || m < 0 || q < 0 || p < 0 || count > 65535 ||
+      (count > 0 && m > 0 && p > 0 && (!out || ((!a || !b) && q > 0)))) {
+    set_status(st, BTD_ERR_INVALID_ARGUMENT, "btd_gemm_batch: bad arguments (at most 65535 members per call)");
+    return BTD_ERR_INVALID_ARGUMENT;
+  }
+  if (count == 0 || m == 0 || p == 0) return BTD_OK;
+  btd::Strides as = to_strides(astrides), bs = to_strides(bstrides);
+  if (trans_a) std::swap(as.r, as.c);  // op(a)(r, k) = a(k, r)
+  if (trans_b) std::swap(bs.r, bs.c);
+  const int tiles_m = (int)((m + btd::kSeamTile - 1) / btd::kSeamTile), tiles_p = (int)((p + btd::kSeamTile - 1) / btd::kSeamTile);
+  dim3 grid((unsigned)(tiles_m * tiles_p), (unsigned)count);
+  btd::seam_gemm_kernel<<<grid, btd::kSeamThreads, 0, (cudaStream_t)stream>>>(
+      out, to_strides(ostrides), a, as, b, bs, (int)m, (int)q, (int)p, tiles_p, alpha, beta);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BTD_OK : cuda_fail(st, e, "btd_gemm_batch");
 }
 
 }  // extern "C"
