@@ -17,6 +17,7 @@
 
 #include "btd_factor.cuh"
 #include "btd_factor3.cuh"
+#include "btd_pair.cuh"
 #include "btd_solve.cuh"
 #include "btd_solve2.cuh"
 #include "btd_solve3.cuh"
@@ -250,6 +251,29 @@ cudaError_t launch_stream64(const btd::FactorArgs& a, unsigned grid, cudaStream_
   return cudaGetLastError();
 }
 
+// Pair-slot schedule (btd_pair.cuh) at NT = 64 on wide coupled levels: one persistent CTA per SM
+// with two segments in flight (pivot chain of one on SMSP 0, the DMMA work of the other on SMSPs
+// 1-3).  Built with -DBTD_NO_PAIR for A/B timing against factor_level_kernel.
+bool use_pair(int nt, const btd::FactorArgs& a) {
+#ifdef BTD_NO_PAIR
+  return false;
+#else
+  const int k = (a.kend ? a.kend : a.K) - a.k0;
+  return nt == 64 && !a.base && k >= 2 * device_sms();
+#endif
+}
+
+cudaError_t launch_pair(const btd::FactorArgs& a, cudaStream_t s) {
+  using PS = btd::PairShape;
+  cudaError_t e = ensure_smem((const void*)btd::factor_pair_kernel, PS::SMEM);
+  if (e != cudaSuccess) return e;
+  const int k = (a.kend ? a.kend : a.K) - a.k0;
+  const unsigned grid = (unsigned)std::min<int>(device_sms(), (k + 1) / 2);
+  btd::factor_pair_kernel<<<grid, PS::NTHREADS, PS::SMEM, s>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
 // Register-resident small-block kernel (btd_small.cuh) at NT = 8.
 bool use_small(int nt) { return nt == 8; }
 
@@ -259,6 +283,7 @@ cudaError_t dispatch_factor(int nt, const btd::FactorArgs& a, unsigned grid, cud
     btd::factor_small_kernel<<<g, btd::kSmallThreads, 0, s>>>(a); g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
   }
+  if (use_pair(nt, a)) return launch_pair(a, s);
   if (use_stream(nt, a)) return launch_stream64(a, grid, s);
   switch (nt) {
     case 8: return launch_factor<8>(a, grid, s);

@@ -1,0 +1,144 @@
+// Microbenchmark: single-warp chain_potrf64 (btd_chain.cuh) vs the 4-warp potrf_trtri<64, false>,
+// alone and next to DMMA traffic on chosen warps (which SMSP a warp runs on decides whether its
+// DMMAs delay the pivot chain).  Also checks the result against a host Cholesky.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/chain2_bench tools/chain2_bench.cu
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_2509_03015_b200/csrc/btd_chain.cuh"
+using namespace btd;
+
+constexpr int NT = 64, LD = 68, THREADS = 512;
+
+__device__ bool spams(int warp, int mode) {
+  switch (mode) {
+    case 1: return warp % 4 != 0;            // SMSP 1-3 busy
+    case 2: return warp >= 1;                // every SMSP busy
+    case 4: return warp % 4 == 0 && warp;    // only the chain's SMSP busy
+    case 5: return warp >= 4;                // potrf_trtri next to 12 DMMA warps
+    default: return false;
+  }
+}
+
+__global__ void __launch_bounds__(THREADS, 1) bench(const double* A, double* out, long long* cyc, int mode, int reps,
+                                                    int* warpid_out) {
+  extern __shared__ __align__(16) double smem[];
+  double* DL = smem;
+  __shared__ volatile int done;
+  __shared__ int sf;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  unsigned wid;
+  asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+  if (lane == 0) warpid_out[warp] = (int)wid;
+  long long tot = 0;
+  int piv = 0;
+  double sink = 0.0;
+  for (int r = 0; r < reps; ++r) {
+    for (int e = tid; e < NT * NT; e += THREADS) DL[(e / NT) * LD + e % NT] = A[e];
+    if (tid == 0) done = 0;
+    __syncthreads();
+    const bool chain4 = mode >= 3 && mode != 4;
+    if (!chain4 && warp == 0) {
+      const long long t0 = clock64();
+      piv = chain_potrf64<LD, NT>(DL, lane);
+      __syncwarp();
+      const long long t1 = clock64();
+      tot += t1 - t0;
+      if (lane == 0) done = 1;
+    } else if (chain4 && warp < 4) {
+      const long long t0 = clock64();
+      piv = potrf_trtri<NT, false>(DL, &sf);
+      named_sync(kBarA, 128);
+      const long long t1 = clock64();
+      tot += t1 - t0;
+      if (tid == 0) done = 1;
+    } else if (spams(warp, mode)) {
+      double a0[2] = {1.0, 1.0}, a1[2] = {1.0, 1.0}, a2[2] = {1.0, 1.0}, a3[2] = {1.0, 1.0};
+      const double x = 1e-3 * lane, y = 2e-3;
+      while (!done) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          dmma(a0, x, y);
+          dmma(a1, x, y);
+          dmma(a2, x, y);
+          dmma(a3, x, y);
+        }
+      }
+      sink += a0[0] + a1[1] + a2[0] + a3[1];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < NT * (LD); e += THREADS) out[e] = DL[e];
+  if (tid == 0) {
+    cyc[0] = tot / reps;
+    cyc[1] = piv;
+  }
+  if (sink == 12345.0) out[0] = sink;
+}
+
+int main() {
+  std::vector<double> M(NT * NT), A(NT * NT), L(NT * NT, 0.0);
+  srand(3);
+  for (auto& v : M) v = rand() / (double)RAND_MAX - 0.5;
+  for (int i = 0; i < NT; ++i)
+    for (int j = 0; j < NT; ++j) {
+      double s = 0;
+      for (int k = 0; k < NT; ++k) s += M[i * NT + k] * M[j * NT + k];
+      A[i * NT + j] = s + (i == j ? NT : 0);
+    }
+  // host Cholesky
+  for (int j = 0; j < NT; ++j) {
+    double s = A[j * NT + j];
+    for (int k = 0; k < j; ++k) s -= L[j * NT + k] * L[j * NT + k];
+    L[j * NT + j] = sqrt(s);
+    for (int i = j + 1; i < NT; ++i) {
+      double t = A[i * NT + j];
+      for (int k = 0; k < j; ++k) t -= L[i * NT + k] * L[j * NT + k];
+      L[i * NT + j] = t / L[j * NT + j];
+    }
+  }
+  // expected output: off-diagonal tiles = L, diagonal tiles = inverse of L's tile
+  std::vector<double> W(NT * NT, 0.0);
+  for (int i = 0; i < NT; ++i)
+    for (int j = 0; j < NT; ++j) W[i * NT + j] = (j < i / 8 * 8) ? L[i * NT + j] : 0.0;
+  for (int p = 0; p < 8; ++p)
+    for (int c = 0; c < 8; ++c) {
+      double x[8] = {0};
+      x[c] = 1.0 / L[(8 * p + c) * NT + 8 * p + c];
+      for (int i = c + 1; i < 8; ++i) {
+        double s = 0;
+        for (int m = c; m < i; ++m) s += L[(8 * p + i) * NT + 8 * p + m] * x[m];
+        x[i] = -s / L[(8 * p + i) * NT + 8 * p + i];
+      }
+      for (int i = 0; i < 8; ++i) W[(8 * p + i) * NT + 8 * p + c] = x[i];
+    }
+  double *dA, *dO;
+  long long* cyc;
+  int* wid;
+  cudaMalloc(&dA, NT * NT * 8);
+  cudaMalloc(&dO, NT * LD * 8);
+  cudaMallocManaged(&cyc, 16);
+  cudaMallocManaged(&wid, 64 * 4);
+  cudaMemcpy(dA, A.data(), NT * NT * 8, cudaMemcpyHostToDevice);
+  const int smem = NT * LD * 8;
+  cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const char* names[] = {"chain1 alone", "chain1 + DMMA on SMSP1-3 (w%4!=0)", "chain1 + DMMA on all other warps",
+                         "potrf_trtri4 alone", "chain1 + DMMA on w%4==0 only", "potrf_trtri4 + DMMA on warps 4-15"};
+  std::vector<double> O(NT * LD);
+  for (int mode = 0; mode < 6; ++mode) {
+    bench<<<1, THREADS, smem>>>(dA, dO, cyc, mode, 3, wid);
+    bench<<<1, THREADS, smem>>>(dA, dO, cyc, mode, 20, wid);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(O.data(), dO, NT * LD * 8, cudaMemcpyDeviceToHost);
+    double err = 0;
+    for (int i = 0; i < NT; ++i)
+      for (int j = 0; j <= i; ++j) err = fmax(err, fabs(O[i * LD + j] - W[i * NT + j]) / fabs(W[i * NT + i / 8 * 8 + i % 8] + 1e-300) * 0 + fabs(O[i * LD + j] - W[i * NT + j]));
+    printf("{\"mode\":%d,\"name\":\"%s\",\"cycles\":%lld,\"fail\":%lld,\"max_abs_err\":%.3e,\"cuda\":\"%s\"}\n", mode,
+           names[mode], cyc[0], cyc[1], err, cudaGetErrorString(e));
+  }
+  printf("{\"warpid_of_warp\":[");
+  for (int w = 0; w < 16; ++w) printf("%d%s", wid[w], w < 15 ? "," : "]}\n");
+  return 0;
+}
