@@ -17,8 +17,11 @@
 
 namespace btd {
 
+// leaf_bars (optional): panel p's mbarrier is arrived on once its leaf and the rows below it are in
+// shared memory (a streaming consumer may start that column block of its triangular solve); on a
+// failure every remaining barrier is arrived on so no consumer waits forever.
 template <int LD, int NT>
-__device__ __forceinline__ int chain_potrf64(double* DL, int lane) {
+__device__ __forceinline__ int chain_potrf64(double* DL, int lane, unsigned long long* leaf_bars = nullptr) {
   static_assert(NT == 64, "chain_potrf64 factors 64 x 64 tiles");
   int fail = 0;
 #pragma unroll
@@ -64,7 +67,11 @@ __device__ __forceinline__ int chain_potrf64(double* DL, int lane) {
         for (int j = k + 1; j <= i; ++j)
           if (!(i == k + 1 && j == k + 1)) a[i][j] = fma(-t[i], a[j][k], a[i][j]);
     }
-    if (fail) return fail;  // uniform over the warp (every lane factored the same tile)
+    if (fail) {  // uniform over the warp (every lane factored the same tile)
+      if (leaf_bars && lane == 0)
+        for (int q = p; q < 8; ++q) mbar_arrive(&leaf_bars[q]);
+      return fail;
+    }
     double lt[8][8];  // L_pp (normalized)
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -118,6 +125,10 @@ __device__ __forceinline__ int chain_potrf64(double* DL, int lane) {
       DL[(p0 + c) * LD + NT] = rinv[c];
     }
     __syncwarp();
+    if (leaf_bars && lane == 0) {
+      __threadfence_block();
+      mbar_arrive(&leaf_bars[p]);
+    }
   }
   return 0;
 }
