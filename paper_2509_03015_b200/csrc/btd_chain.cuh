@@ -11,9 +11,8 @@
 // (left-looking never reads a finished diagonal tile, so the leaves can be written at once).
 // Failure rule as everywhere: a pivot that is not > 0 (NaN included) -> 1-based pivot returned,
 // the block's contents are then undefined.
+// Included by btd_factor.cuh after the helpers it uses (dmma, sub_frag, rcp_nr, rsqrt_nr).
 #pragma once
-
-#include "btd_factor.cuh"
 
 namespace btd {
 
@@ -21,26 +20,27 @@ namespace btd {
 // shared memory (a streaming consumer may start that column block of its triangular solve); on a
 // failure every remaining barrier is arrived on so no consumer waits forever.
 template <int LD, int NT>
-__device__ __forceinline__ int chain_potrf64(double* DL, int lane, unsigned long long* leaf_bars = nullptr) {
-  static_assert(NT == 64, "chain_potrf64 factors 64 x 64 tiles");
+__device__ __forceinline__ int chain_potrf(double* DL, int lane, unsigned long long* leaf_bars = nullptr) {
+  static_assert(NT == 32 || NT == 64, "chain_potrf factors 32 x 32 or 64 x 64 tiles");
+  constexpr int NP = NT / 8;
   int fail = 0;
 #pragma unroll
-  for (int p = 0; p < 8; ++p) {
+  for (int p = 0; p < NP; ++p) {
     const int p0 = 8 * p;
     // ---- 1. left-looking update of panel p by panels 0..p-1 ----
     if (p > 0) {
-      double acc[8][2];
+      double acc[NP][2];
 #pragma unroll
-      for (int tr = p; tr < 8; ++tr) acc[tr][0] = acc[tr][1] = 0.0;
+      for (int tr = p; tr < NP; ++tr) acc[tr][0] = acc[tr][1] = 0.0;
       const double* pb = DL + (p0 + (lane >> 2)) * LD + (lane & 3);
 #pragma unroll
       for (int k0 = 0; k0 < p0; k0 += 4) {
         const double b = pb[k0];
 #pragma unroll
-        for (int tr = p; tr < 8; ++tr) dmma(acc[tr], DL[(tr * 8 + (lane >> 2)) * LD + k0 + (lane & 3)], b);
+        for (int tr = p; tr < NP; ++tr) dmma(acc[tr], DL[(tr * 8 + (lane >> 2)) * LD + k0 + (lane & 3)], b);
       }
 #pragma unroll
-      for (int tr = p; tr < 8; ++tr) sub_frag<LD>(DL, tr, p, lane, acc[tr]);
+      for (int tr = p; tr < NP; ++tr) sub_frag<LD>(DL, tr, p, lane, acc[tr]);
       __syncwarp();
     }
     // ---- 2. redundant factorization of the diagonal tile ----
@@ -69,7 +69,7 @@ __device__ __forceinline__ int chain_potrf64(double* DL, int lane, unsigned long
     }
     if (fail) {  // uniform over the warp (every lane factored the same tile)
       if (leaf_bars && lane == 0)
-        for (int q = p; q < 8; ++q) mbar_arrive(&leaf_bars[q]);
+        for (int q = p; q < NP; ++q) mbar_arrive(&leaf_bars[q]);
       return fail;
     }
     double lt[8][8];  // L_pp (normalized)
@@ -81,7 +81,7 @@ __device__ __forceinline__ int chain_potrf64(double* DL, int lane, unsigned long
     }
     // ---- 3. rows below the tile: l = x L_pp^{-T} (forward substitution) ----
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < NT / 32; ++h) {
       const int r = p0 + 8 + lane + 32 * h;
       if (r < NT) {
         double x[8];
@@ -131,6 +131,11 @@ __device__ __forceinline__ int chain_potrf64(double* DL, int lane, unsigned long
     }
   }
   return 0;
+}
+
+template <int LD, int NT>
+__device__ __forceinline__ int chain_potrf64(double* DL, int lane, unsigned long long* leaf_bars = nullptr) {
+  return chain_potrf<LD, NT>(DL, lane, leaf_bars);
 }
 
 }  // namespace btd

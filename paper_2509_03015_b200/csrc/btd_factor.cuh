@@ -256,6 +256,10 @@ __device__ __forceinline__ void tile_update(double* DL, int tr, int tc, int p0, 
   sub_frag<LD>(DL, tr, tc, lane, acc);
 }
 
+}  // namespace btd
+#include "btd_chain.cuh"
+namespace btd {
+
 // Rank-8 updates by the panel at column p0 of the lower-triangular tile set
 // {(off + tr, off + tc) : 0 <= tc <= tr < m}, units u = first, first + step, ...  Processed in
 // batches of B tiles with every fragment load issued before the DMMAs (ILP: one tile's
@@ -287,6 +291,72 @@ __device__ __forceinline__ void tile_update_tri(double* DL, int off, int m, int 
       dmma(acc, a0[q], b0[q]);
       dmma(acc, a1[q], b1[q]);
       sub_frag<LD>(DL, tr[q], tc[q], lane, acc);
+    }
+  }
+}
+
+
+// Recursive doubling on DMMA, run by the NWA warps of group A (named barrier kBarA), turning
+// L with inverted 8x8 diagonal tiles into the full inverse Linv, in place:
+//   [[A,0],[B,C]]^{-1} = [[Ai,0],[-Ci B Ai, Ci]]   for blocks of 8, 16, 32 rows.
+template <int NT>
+__device__ __forceinline__ void trtri_doubling(double* DL, int warp, int lane) {
+  using S = FactorShape<NT>;
+  constexpr int LD = S::LD;
+  constexpr int NWA = S::NWA;
+  constexpr int MAXV = S::MAXV;
+
+  // ---- recursive doubling: [[A,0],[B,C]]^{-1} = [[Ai,0],[-Ci B Ai, Ci]] on DMMA ----
+#pragma unroll
+  for (int b = 8; 2 * b <= NT; b *= 2) {
+    const int tpb = b / 8;
+    const int units = (NT / (2 * b)) * tpb * tpb;
+#pragma unroll
+    for (int phase = 0; phase < 2; ++phase) {
+      double acc[MAXV][2];
+      int i0v[MAXV], trv[MAXV], tcv[MAXV];
+      bool ok[MAXV];
+#pragma unroll
+      for (int q = 0; q < MAXV; ++q) {
+        const int u = warp + q * NWA;
+        ok[q] = u < units;
+        const int pair = u / (tpb * tpb), rem = u % (tpb * tpb);
+        i0v[q] = pair * 2 * b;
+        trv[q] = rem / tpb;
+        tcv[q] = rem % tpb;
+        acc[q][0] = acc[q][1] = 0.0;
+      }
+      for (int k0 = 0; k0 < b; k0 += 4) {
+#pragma unroll
+        for (int q = 0; q < MAXV; ++q) {
+          if (!ok[q]) continue;
+          const int i0 = i0v[q];
+          if (phase == 0) {  // T = B * Ainv  (Ainv[k][c] == 0 for k < c)
+            if (k0 < tcv[q] * 8) continue;
+            const double a = DL[(i0 + b + trv[q] * 8 + (lane >> 2)) * LD + i0 + k0 + (lane & 3)];
+            const double bb = DL[(i0 + k0 + (lane & 3)) * LD + i0 + tcv[q] * 8 + (lane >> 2)];
+            dmma(acc[q], a, bb);
+          } else {  // B <- -Cinv * T  (Cinv[r][k] == 0 for k > r)
+            if (k0 > trv[q] * 8 + 4) continue;
+            const double a = DL[(i0 + b + trv[q] * 8 + (lane >> 2)) * LD + i0 + b + k0 + (lane & 3)];
+            const double bb = DL[(i0 + k0 + (lane & 3)) * LD + i0 + b + tcv[q] * 8 + (lane >> 2)];
+            dmma(acc[q], a, bb);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < MAXV; ++q) {
+        if (!ok[q]) continue;
+        const int i0 = i0v[q];
+        if (phase == 0) {  // strictly-upper scratch block (rows i0.., cols i0+b..)
+          double* dst = DL + (i0 + trv[q] * 8 + (lane >> 2)) * LD + i0 + b + tcv[q] * 8 + 2 * (lane & 3);
+          *reinterpret_cast<double2*>(dst) = make_double2(acc[q][0], acc[q][1]);
+        } else {
+          double* dst = DL + (i0 + b + trv[q] * 8 + (lane >> 2)) * LD + i0 + tcv[q] * 8 + 2 * (lane & 3);
+          *reinterpret_cast<double2*>(dst) = make_double2(-acc[q][0], -acc[q][1]);
+        }
+      }
+      named_sync(kBarA, NWA * 32);
     }
   }
 }
@@ -369,60 +439,7 @@ __device__ int potrf_trtri(double* DL, int* s_fail, unsigned long long* leaf_bar
   } else {
   named_sync(kBarA, NWA * 32);
   BTD_PHASE(9);
-
-  // ---- recursive doubling: [[A,0],[B,C]]^{-1} = [[Ai,0],[-Ci B Ai, Ci]] on DMMA ----
-#pragma unroll
-  for (int b = 8; 2 * b <= NT; b *= 2) {
-    const int tpb = b / 8;
-    const int units = (NT / (2 * b)) * tpb * tpb;
-#pragma unroll
-    for (int phase = 0; phase < 2; ++phase) {
-      double acc[MAXV][2];
-      int i0v[MAXV], trv[MAXV], tcv[MAXV];
-      bool ok[MAXV];
-#pragma unroll
-      for (int q = 0; q < MAXV; ++q) {
-        const int u = warp + q * NWA;
-        ok[q] = u < units;
-        const int pair = u / (tpb * tpb), rem = u % (tpb * tpb);
-        i0v[q] = pair * 2 * b;
-        trv[q] = rem / tpb;
-        tcv[q] = rem % tpb;
-        acc[q][0] = acc[q][1] = 0.0;
-      }
-      for (int k0 = 0; k0 < b; k0 += 4) {
-#pragma unroll
-        for (int q = 0; q < MAXV; ++q) {
-          if (!ok[q]) continue;
-          const int i0 = i0v[q];
-          if (phase == 0) {  // T = B * Ainv  (Ainv[k][c] == 0 for k < c)
-            if (k0 < tcv[q] * 8) continue;
-            const double a = DL[(i0 + b + trv[q] * 8 + (lane >> 2)) * LD + i0 + k0 + (lane & 3)];
-            const double bb = DL[(i0 + k0 + (lane & 3)) * LD + i0 + tcv[q] * 8 + (lane >> 2)];
-            dmma(acc[q], a, bb);
-          } else {  // B <- -Cinv * T  (Cinv[r][k] == 0 for k > r)
-            if (k0 > trv[q] * 8 + 4) continue;
-            const double a = DL[(i0 + b + trv[q] * 8 + (lane >> 2)) * LD + i0 + b + k0 + (lane & 3)];
-            const double bb = DL[(i0 + k0 + (lane & 3)) * LD + i0 + b + tcv[q] * 8 + (lane >> 2)];
-            dmma(acc[q], a, bb);
-          }
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < MAXV; ++q) {
-        if (!ok[q]) continue;
-        const int i0 = i0v[q];
-        if (phase == 0) {  // strictly-upper scratch block (rows i0.., cols i0+b..)
-          double* dst = DL + (i0 + trv[q] * 8 + (lane >> 2)) * LD + i0 + b + tcv[q] * 8 + 2 * (lane & 3);
-          *reinterpret_cast<double2*>(dst) = make_double2(acc[q][0], acc[q][1]);
-        } else {
-          double* dst = DL + (i0 + b + trv[q] * 8 + (lane >> 2)) * LD + i0 + tcv[q] * 8 + 2 * (lane & 3);
-          *reinterpret_cast<double2*>(dst) = make_double2(-acc[q][0], -acc[q][1]);
-        }
-      }
-      named_sync(kBarA, NWA * 32);
-    }
-  }
+  trtri_doubling<NT>(DL, warp, lane);
   BTD_PHASE(10);
   return 0;
   }
@@ -572,7 +589,7 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
   extern __shared__ __align__(16) double smem[];
   double* XP = smem;                // 2NT x LD : [X1 | Pt1] rows 0..NT-1, [Gt | Pt2] rows NT..2NT-1
   double* DL = smem + 2 * NT * LD;  // NT x LD  : D -> L -> Linv
-  __shared__ int s_fail;
+  __shared__ int s_fail, s_fail_a;
 
   const int k = args.k0 + blockIdx.x;
   if (npd_superseded(args.err, args.level, 0, k)) return;
@@ -608,7 +625,26 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
     const bool last = (j == J - 1);
     // ================= phase 1: A factors D_j ; B finishes step j-1 =================
     int fail = 0;
-    if (in_a) fail = potrf_trtri<NT>(DL, &s_fail);
+#ifdef BTD_R1_CHAIN
+    constexpr bool kChain = false;  // A/B builds: the round-1 four-warp potrf_trtri
+#else
+    constexpr bool kChain = NT >= 32;
+#endif
+    if constexpr (kChain) {
+      // single-warp left-looking pivot chain (btd_chain.cuh), then the inverse by recursive
+      // doubling on the whole of group A
+      if (in_a) {
+        if (warp == 0) {
+          const int f = chain_potrf<LD, NT>(DL, lane);
+          if (lane == 0) s_fail_a = f;
+        }
+        named_sync(kBarA, NWA * 32);
+        fail = s_fail_a;
+        if (!fail) trtri_doubling<NT>(DL, warp, lane);
+      }
+    } else {
+      if (in_a) fail = potrf_trtri<NT>(DL, &s_fail);
+    }
     if (NWB == 0) __syncthreads();  // single-warp CTA: group B work runs after the factor
     constexpr int SKIPB = 0;
     if (j > 0 && (NWB == 0 || (!in_a && wb >= SKIPB))) {

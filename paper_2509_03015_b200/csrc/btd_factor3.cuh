@@ -23,7 +23,6 @@
 // Per step the critical path is the pivot chain + one column block of the solve + the D update.
 #pragma once
 
-#include "btd_chain.cuh"
 #include "btd_factor.cuh"
 
 namespace btd {
@@ -198,7 +197,7 @@ __global__ void __launch_bounds__(StreamShape::NTHREADS, 1) factor_stream_kernel
     const long long tstep = clock64();
     if (in_a) {
       // ======== group A: Cholesky of D_j, leaves published one by one ========
-#ifdef BTD_STREAM_CHAIN4
+#ifdef BTD_R1_CHAIN
       const int fail = potrf_trtri<NT, false>(DL, &s_fail_a, leaf_bar);
 #else
       // single-warp left-looking chain (btd_chain.cuh): no group barriers on the critical path

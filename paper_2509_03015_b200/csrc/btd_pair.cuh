@@ -21,7 +21,6 @@
 // Phase t: slot t % 2 is the chain slot, the other the bulk slot; __syncthreads ends a phase.
 #pragma once
 
-#include "btd_chain.cuh"
 #include "btd_factor3.cuh"
 
 namespace btd {

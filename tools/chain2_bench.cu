@@ -7,7 +7,7 @@
 #include <cstdlib>
 #include <vector>
 
-#include "../paper_2509_03015_b200/csrc/btd_chain.cuh"
+#include "../paper_2509_03015_b200/csrc/btd_factor.cuh"
 using namespace btd;
 
 constexpr int NT = 64, LD = 68, THREADS = 512;
