@@ -457,10 +457,13 @@ def run_sharded(args, rank, world):
     def step(d_, s_, b_):
         solver.factorize(d_, s_)
         x = solver.solve(b_)
-        solver.engine.release(solver.state)
+        solver.engine.release(solver.state)  # one partial factor alive at a time (config 5 is large)
+        solver.reduced = None
         return x
 
+    x = None
     for _ in range(max(args.warmup, 3)):
+        x = None
         x = step(dd, ds, db)
     torch.cuda.synchronize()
     rres = sharded_residual(plan, rank, dd, ds, db, x, dist)
@@ -476,6 +479,7 @@ def run_sharded(args, rank, world):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ev[0].record(stream)
     for _ in range(args.steps):
+        x = None
         x = step(dd, ds, db)
     ev[1].record(stream)
     torch.cuda.synchronize()
@@ -488,12 +492,16 @@ def run_sharded(args, rank, world):
     clocks = sampler.stop(dev.index) if sampler else None
 
     # end to end: pinned host chunk -> device -> sharded factor + solve -> host solution chunk
+    x = None
+    del dd, ds, db
+    torch.cuda.empty_cache()  # the e2e leg copies its own device chunk (config 5: 34 GB per rank at N=2)
     hx = torch.empty_like(hb)
     dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     e2e_steps = max(1, args.steps // 2)
     for _ in range(e2e_steps):
+        xx = None
         xx = step(hd.to(dev, non_blocking=True), hs.to(dev, non_blocking=True), hb.to(dev, non_blocking=True))
         hx.copy_(xx)
     torch.cuda.synchronize()

@@ -281,9 +281,13 @@ class CudaEngine:
         return recursive_solve(h, BlockRhs(rhs.contiguous())).blocks
 
     def release(self, state):
+        """Drop this rank's partial factor (C handle and device buffers); the solution returned by
+        solve_up stays valid."""
         if state.get("h"):
             _native.lib().btd_destroy(state["h"])
             state["h"] = None
+        for key in ("pers", "scr", "x"):
+            state.pop(key, None)
 
 
 # ------------------------------------------------------------------------------------------
