@@ -1,0 +1,10 @@
+#!/bin/bash
+# small-block factor kernel v2 (shared-memory broadcasts): parity + A/B timing vs v1
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_graphs.py -q -x -p no:cacheprovider > gpurun_out/c_pytest.log 2>&1
+echo "rc=$?" >> gpurun_out/c_pytest.log
+for lib in paper_2509_03015_b200/libblocktri_b200.so tools/lib_s2_3.so tools/lib_s1.so; do
+  echo "== $lib" >> gpurun_out/c_time.log
+  BTD_LIB=$lib timeout 300 python tools/quick_time.py 1048576,8,1 200000,5,2 >> gpurun_out/c_time.log 2>&1
+  BTD_LIB=$lib timeout 300 python tools/level_times.py 1048576,8,1 >> gpurun_out/c_time.log 2>&1
+done
