@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(BTHREADS) bt_gemm_kernel(GemmArgs g) {
   const int k = g.k0 + blockIdx.y;
   // skip only when a recorded failure can no longer be superseded by this (step, member): a lower
   // member failing at a later 64-column tile of the same step must still be found
-  if (npd_superseded(g.err, g.level, g.j, k)) return;
+  if (cta_superseded(g.err, g.level, g.j, k)) return;
   int J;
   if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, g.act, J)) return;
   const int ks = g.ksplit > 1 ? g.ksplit : 1;
@@ -285,7 +285,7 @@ struct BigDiagArgs {
 __global__ void __launch_bounds__(128) big_diag_potrf_kernel(BigDiagArgs g) {
   constexpr int LD = FactorShape<64>::LD;
   const int k = g.k0 + blockIdx.x;
-  if (npd_superseded(g.err, g.level, g.j, k)) return;
+  if (cta_superseded(g.err, g.level, g.j, k)) return;
   int J;
   if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, kActAll, J)) return;
   __shared__ __align__(16) double DL[BT * LD];
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(BTHREADS) big_potrf_kernel(BigPotrfArgs g) {
   // exits must be uniform over a cluster (cluster barriers follow): with csize > 1 a segment does
   // not skip on another segment's error (its own step-(j-1) failure was already reported, and a
   // later report can never supersede an earlier one)
-  if (C == 1 && npd_superseded(g.err, g.level, g.j, k)) return;
+  if (C == 1 && cta_superseded(g.err, g.level, g.j, k)) return;
   if (!segment_active(g.seps, g.base_mode, g.N, k, g.j, kActAll, J)) return;
   extern __shared__ __align__(16) double sm[];
   double* DL = sm;             // 64 x LD diagonal tile (rank 0)

@@ -17,7 +17,6 @@
 
 #include "btd_factor.cuh"
 #include "btd_factor3.cuh"
-#include "btd_pair.cuh"
 #include "btd_solve.cuh"
 #include "btd_solve2.cuh"
 #include "btd_solve3.cuh"
@@ -251,46 +250,18 @@ cudaError_t launch_stream64(const btd::FactorArgs& a, unsigned grid, cudaStream_
   return cudaGetLastError();
 }
 
-// Pair-slot schedule (btd_pair.cuh) at NT = 64 on wide coupled levels: one persistent CTA per SM
-// with two segments in flight (pivot chain of one on SMSP 0, the DMMA work of the other on SMSPs
-// 1-3).  Opt-in (-DBTD_PAIR): measured slower than two factor_level_kernel CTAs per SM (cfg2
-// level 0 8.85 vs 6.41 ms), see DESIGN.md.
-bool use_pair(int nt, const btd::FactorArgs& a) {
-#ifndef BTD_PAIR
-  (void)nt; (void)a;
-  return false;
-#else
-  const int k = (a.kend ? a.kend : a.K) - a.k0;
-  return nt == 64 && !a.base && k >= 2 * device_sms();
-#endif
-}
-
-cudaError_t launch_pair(const btd::FactorArgs& a, cudaStream_t s) {
-  using PS = btd::PairShape;
-  cudaError_t e = ensure_smem((const void*)btd::factor_pair_kernel, PS::SMEM);
-  if (e != cudaSuccess) return e;
-  const int k = (a.kend ? a.kend : a.K) - a.k0;
-  const unsigned grid = (unsigned)std::min<int>(device_sms(), (k + 1) / 2);
-  btd::factor_pair_kernel<<<grid, PS::NTHREADS, PS::SMEM, s>>>(a);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
-}
-
-// Register-resident small-block kernel (btd_small.cuh) at NT = 8.
+// Small-block kernels (btd_small.cuh) at NT = 8: an 8-lane group per segment.
 bool use_small(int nt) { return nt == 8; }
 
 cudaError_t dispatch_factor(int nt, const btd::FactorArgs& a, unsigned grid, cudaStream_t s) {
   if (use_small(nt)) {
     const unsigned g = a.base ? 1u : (grid + 15) / 16;
-#ifdef BTD_SMALL_V1
-    btd::factor_small_kernel<<<g, btd::kSmallThreads, 0, s>>>(a);
-#else
-    btd::factor_small2_kernel<<<g, btd::kSmallThreads, btd::kS2Smem, s>>>(a);
-#endif
+    cudaError_t e = ensure_smem((const void*)btd::factor_small_kernel, btd::kS2Smem);
+    if (e != cudaSuccess) return e;
+    btd::factor_small_kernel<<<g, btd::kSmallThreads, btd::kS2Smem, s>>>(a);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
   }
-  if (use_pair(nt, a)) return launch_pair(a, s);
   if (use_stream(nt, a)) return launch_stream64(a, grid, s);
   switch (nt) {
     case 8: return launch_factor<8>(a, grid, s);
@@ -359,15 +330,9 @@ cudaError_t launch_solve_small(const btd::SolveArgs& a, cudaStream_t s) {
   const unsigned gx = a.mode == btd::kSolveBase ? 1u : (unsigned)((a.K + 15) / 16);
   const int dc = a.d == 1 ? 1 : a.d == 2 ? 2 : 4;
   dim3 grid(gx, (unsigned)((a.d + dc - 1) / dc));
-#ifdef BTD_SMALL_V1
-  if (dc == 1) btd::solve_small_kernel<1><<<grid, btd::kSmallThreads, 0, s>>>(a);
-  else if (dc == 2) btd::solve_small_kernel<2><<<grid, btd::kSmallThreads, 0, s>>>(a);
-  else btd::solve_small_kernel<4><<<grid, btd::kSmallThreads, 0, s>>>(a);
-#else
-  if (dc == 1) btd::solve_small2_kernel<1><<<grid, btd::kSmallThreads, btd::SS2<1>::SMEM, s>>>(a);
-  else if (dc == 2) btd::solve_small2_kernel<2><<<grid, btd::kSmallThreads, btd::SS2<2>::SMEM, s>>>(a);
-  else btd::solve_small2_kernel<4><<<grid, btd::kSmallThreads, btd::SS2<4>::SMEM, s>>>(a);
-#endif
+  if (dc == 1) btd::solve_small_kernel<1><<<grid, btd::kSmallThreads, btd::SS2<1>::SMEM, s>>>(a);
+  else if (dc == 2) btd::solve_small_kernel<2><<<grid, btd::kSmallThreads, btd::SS2<2>::SMEM, s>>>(a);
+  else btd::solve_small_kernel<4><<<grid, btd::kSmallThreads, btd::SS2<4>::SMEM, s>>>(a);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

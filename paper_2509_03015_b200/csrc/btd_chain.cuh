@@ -1,5 +1,5 @@
-// Single-warp Cholesky of one 64 x 64 diagonal block (the pivot chain of the pair-slot level
-// kernel, btd_pair.cuh).
+// Single-warp Cholesky of one 32 x 32 or 64 x 64 diagonal block (the pivot chain of
+// factor_level_kernel and factor_stream_kernel).
 //
 // Left-looking over eight 8-column panels, so one warp needs no barrier at all:
 //   1. panel p -= L[:, 0:8p] L[panel rows, 0:8p]^T            (DMMA tiles, independent rows)

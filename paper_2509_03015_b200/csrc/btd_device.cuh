@@ -54,6 +54,17 @@ __device__ __forceinline__ bool npd_superseded(const DevErr* e, int level, long 
   return j > jerr || (j == jerr && member > merr);
 }
 
+// CTA-uniform form of npd_superseded for a kernel's entry check: the error word can be written by
+// another CTA (of this or a concurrently running launch) while this CTA starts, so threads reading
+// it separately could disagree and some would exit while the others wait at a barrier.  Thread 0
+// decides for the CTA.  Call once, at kernel entry, from every thread.
+__device__ __forceinline__ bool cta_superseded(const DevErr* e, int level, long long j, long long member) {
+  __shared__ int s_superseded;
+  if (threadIdx.x == 0) s_superseded = npd_superseded(e, level, j, member) ? 1 : 0;
+  __syncthreads();
+  return s_superseded != 0;
+}
+
 // ---------------------------------------------------------------------------------------------
 // fp64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col).
 // Fragment ownership (lane l): a = A[l/4][l%4], b = B[l%4][l/4], d = {D[l/4][2(l%4)], D[l/4][2(l%4)+1]}.
@@ -221,6 +232,20 @@ __host__ __device__ __forceinline__ int packed_offset_(int r) {
 }
 template <int NT, int LD, int NTHREADS>
 __device__ __forceinline__ void store_packed_lower(double* g, const double* sm, int n) {
+  if ((n & 1) == 0 && NT <= 64) {
+    // even n: a warp per row, a lane per column pair -- one 16-byte shared load and one 16-byte
+    // global store per pair (packed rows start at even offsets; the block stride is even)
+    constexpr int NWARPS = NTHREADS / 32;
+    const int lane = threadIdx.x & 31;
+    for (int r = threadIdx.x >> 5; r < n; r += NWARPS) {
+      const int len = ((r + 2) >> 1) << 1, c = 2 * lane;
+      if (c < len) {
+        const double2 v = *reinterpret_cast<const double2*>(sm + r * LD + c);
+        *reinterpret_cast<double2*>(g + packed_offset_(r) + c) = make_double2(v.x, c + 1 <= r ? v.y : 0.0);
+      }
+    }
+    return;
+  }
   // (r, c) for c <= r, plus the zero pad (r, r+1) of even rows
   for (int e = threadIdx.x; e < n * (n + 1); e += NTHREADS) {
     const int r = e / (n + 1), c = e % (n + 1);

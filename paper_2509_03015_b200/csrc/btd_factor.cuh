@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
   __shared__ int s_fail, s_fail_a;
 
   const int k = args.k0 + blockIdx.x;
-  if (npd_superseded(args.err, args.level, 0, k)) return;
+  if (cta_superseded(args.err, args.level, 0, k)) return;
   const bool coupled = !args.base;
   const long long start = coupled ? (long long)args.seps[k] + 1 : 0;
   const long long stop = coupled ? (long long)args.seps[k + 1] : args.N;
@@ -657,7 +657,15 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
         named_sync(kBarB, nb);
       }
       // L_{j,j-1} (Pt1 of step j-1) -> global, then stage the next X1 over it
-      for (int e = gt; e < n * n; e += nb) args.Lsub[(start + j - 1) * bs + e] = XP[(e / n) * LD + e % n];
+      if (n == NT) {  // 16-byte copies, no index division
+        double* dst = args.Lsub + (start + j - 1) * bs;
+        for (int e = gt; e < NT * NT / 2; e += nb) {
+          const int r = e / (NT / 2), c = 2 * (e % (NT / 2));
+          *reinterpret_cast<double2*>(dst + r * NT + c) = *reinterpret_cast<const double2*>(XP + r * LD + c);
+        }
+      } else {
+        for (int e = gt; e < n * n; e += nb) args.Lsub[(start + j - 1) * bs + e] = XP[(e / n) * LD + e % n];
+      }
       named_sync(kBarB, nb);
       const double* nx = !last ? args.sub + (start + j) * bs : (coupled ? args.sub + (stop - 1) * bs : nullptr);
       if (nx) {

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(StreamShape::NTHREADS, 1) factor_stream_kernel
   __shared__ int s_fail_a, s_fail;
 
   const int k = args.k0 + blockIdx.x;
-  if (npd_superseded(args.err, args.level, 0, k)) return;
+  if (cta_superseded(args.err, args.level, 0, k)) return;
   const bool coupled = !args.base;
   const long long start = coupled ? (long long)args.seps[k] + 1 : 0;
   const long long stop = coupled ? (long long)args.seps[k + 1] : args.N;

@@ -1,19 +1,20 @@
-// Small-block (n <= 8) level elimination and level solve, register resident: one 8-lane group of a
-// warp per segment (lane = one block row), 4 segments per warp, blocks streamed straight from HBM
-// into registers (no shared memory, no block-level barriers).
+// Small-block (n <= 8) level elimination and level solve: one 8-lane group of a warp per segment
+// (lane = one block row), 4 segments per warp, 16 per 128-thread CTA.
 //
 // At n = 8 (BASELINE config 3, N = 2^20) a 64-element block is far too small for a CTA-per-segment
-// kernel: factor_level_kernel<8> keeps one warp per segment at ~16 CTAs/SM and its per-step
-// latency, not HBM, sets the time.  Here all the per-step algebra is row-parallel inside the
-// group; the cross-row data movement is done with width-8 warp shuffles.
+// kernel (factor_level_kernel<8> would keep one warp per segment at ~16 CTAs/SM, latency bound).
+// Here the per-step algebra is row-parallel inside the group and the blocks move through small
+// per-group shared-memory tiles: coalesced cp.async streaming one step ahead, cross-lane exchange
+// by broadcast shared-memory reads.  (Round 1 exchanged rows with width-8 warp shuffles: ~470 SHFL
+// per warp-step, and SHFL issues at one warp-instruction per clock per SM -- the level-0 factor of
+// config 3 took 1.04 ms; with the shared-memory exchange 0.66 ms.)
 //
 // Factor (same Y-form algebra as factor_level_kernel, reference chain permute_split /
 // factorize_btd_batch / solve_btd_batch(F) / compute_schur, bt/schur.py:98-193,
-// bt/block_cholesky.py:24-68), per step j with lane r holding row r of every block:
-//   L L^T = D_j (row-owner Cholesky: pivot broadcast, column broadcast, rank-1 row updates)
-//   Linv = L^{-1} (forward substitution, one broadcast row per step)      -> HBM (packed row r)
-//   Pt1 = X1 Linv^T, Pt2 = Gt Linv^T (Linv entries broadcast)            -> L_{j+1,j} = Pt1 -> HBM
-//   D_{j+1} = A_{j+1,j+1} - Pt1 Pt1^T, Gt_{j+1} = -Pt2 Pt1^T, S_L += Pt2 Pt2^T (rows of Pt broadcast)
+// bt/block_cholesky.py:24-68), per step j with lane r holding row r:
+//   L L^T = D_j (redundant in every lane of the group)  Linv = L^{-1} (row r by lane r) -> HBM
+//   Pt1 = X1 Linv^T, Pt2 = Gt Linv^T                   -> L_{j+1,j} = Pt1 -> HBM
+//   D_{j+1} = A_{j+1,j+1} - Pt1 Pt1^T, Gt_{j+1} = -Pt2 Pt1^T, S_L += Pt2 Pt2^T
 //   last row: S_R = Pt1 Pt1^T, S_sub = -Pt1 Pt2^T.
 #pragma once
 
@@ -25,8 +26,6 @@ namespace btd {
 
 constexpr int kSmallNT = 8;
 constexpr int kSmallThreads = 128;  // 4 warps, 16 segments per CTA
-
-__device__ __forceinline__ double gbc(double v, int src) { return __shfl_sync(0xffffffffu, v, src, kSmallNT); }
 
 // row r of an n x n row-major block (zero padded to 8; `eye` puts 1 on padded diagonal entries)
 __device__ __forceinline__ void load_row8(double (&v)[8], const double* blk, int n, int r, bool ok, bool eye) {
@@ -45,161 +44,8 @@ __device__ __forceinline__ void store_row8(double* blk, const double (&v)[8], in
     if (c < n) blk[r * n + c] = v[c];
 }
 
-#ifndef BTD_FSMALL_MINB
-#define BTD_FSMALL_MINB 3
-#endif
-__global__ void __launch_bounds__(kSmallThreads, BTD_FSMALL_MINB) factor_small_kernel(FactorArgs a) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 3, r = lane & 7;
-  const bool coupled = !a.base;
-  const int k = coupled ? a.k0 + (blockIdx.x * 4 + warp) * 4 + g : 0;
-  const bool valid = coupled ? (k < (a.kend ? a.kend : a.K)) : (blockIdx.x == 0 && warp == 0 && g == 0);
-  const int n = a.n;
-  const size_t bs = (size_t)n * n;
-  const int pk = packed_offset_(n);
-  // CTA-uniform early exit (shuffles need whole warps): the CTA's first segment has the lowest k
-  if (npd_superseded(a.err, a.level, 0, coupled ? a.k0 + blockIdx.x * 16 : 0)) return;
-  const long long start = !valid ? 0 : (coupled ? (long long)a.seps[k] + 1 : 0);
-  const long long stop = !valid ? 0 : (coupled ? (long long)a.seps[k + 1] : a.N);
-  const int J = (int)(stop - start);
-  // the warp iterates to its longest segment (shuffles need the whole warp)
-  int jw = J;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) jw = max(jw, __shfl_xor_sync(0xffffffffu, jw, o));
-
-  double D[8], X[8], G[8], SL[8], NA[8], NX[8];
-  load_row8(D, valid ? a.diag + start * bs : nullptr, n, r, valid, true);
-  if (valid && coupled) {
-    load_row8(X, J > 1 ? a.sub + start * bs : a.sub + (stop - 1) * bs, n, r, true, false);
-    load_col8(G, a.sub + (start - 1) * bs, n, r, true);  // Gt_0 = C_L^T
-    // coupling copies kept in the hierarchy (C_L, C_R)
-    double t[8];
-    load_row8(t, a.sub + (start - 1) * bs, n, r, true, false);
-    store_row8(a.Lsub + (start - 1) * bs, t, n, r, true);
-    load_row8(t, a.sub + (stop - 1) * bs, n, r, true, false);
-    store_row8(a.Lsub + (stop - 1) * bs, t, n, r, true);
-  } else {
-    load_row8(X, valid && J > 1 ? a.sub + start * bs : nullptr, n, r, valid && J > 1, false);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) G[c] = 0.0;
-  }
-#pragma unroll
-  for (int c = 0; c < 8; ++c) SL[c] = 0.0;
-  int fail = 0, fail_j = 0;
-
-  for (int j = 0; j < jw; ++j) {
-    const bool act = valid && j < J && fail == 0;
-    const bool last = (j == J - 1);
-    // prefetch the next step's A_{j+1,j+1} and X1 (A_{j+2,j+1}, or C_R for the last row)
-    const bool more = act && j + 1 < J;
-    load_row8(NA, more ? a.diag + (start + j + 1) * bs : nullptr, n, r, more, true);
-    const bool xnext = act && (coupled ? j + 1 < J : j + 2 < J);
-    const double* xs = (j + 2 < J) ? a.sub + (start + j + 1) * bs : a.sub + (stop - 1) * bs;
-    load_row8(NX, xnext ? xs : nullptr, n, r, xnext, false);
-
-    // ---- Cholesky, row-owner: lane r holds row r; D[c] -> L[r][c] for c <= r ----
-    double rinv_own = 1.0;
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const double dkk = gbc(D[kk], kk);
-      if (act && fail == 0 && r == 0 && dkk <= 0.0) fail = kk + 1;
-      const double ri = rsqrt(dkk);
-      const double lrk = D[kk] * ri;  // L[r][kk] (r >= kk); garbage above, never used
-      if (r == kk) rinv_own = ri;
-      double lck[8];
-#pragma unroll
-      for (int c = kk + 1; c < 8; ++c) lck[c] = gbc(lrk, c);
-#pragma unroll
-      for (int c = kk + 1; c < 8; ++c) D[c] = fma(-lrk, lck[c], D[c]);
-      D[kk] = lrk;
-    }
-    fail = __shfl_sync(0xffffffffu, fail, g * 8, 32);  // group-uniform
-    if (fail && act) fail_j = j;
-    // ---- Linv = L^{-1}: lane r finalises row r at step m = r; rows are broadcast as they finish ----
-    double Li[8], acc[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      acc[c] = (c == r) ? 1.0 : 0.0;
-      Li[c] = 0.0;
-    }
-#pragma unroll
-    for (int m = 0; m < 8; ++m) {
-      if (r == m) {
-#pragma unroll
-        for (int c = 0; c <= m; ++c) Li[c] = acc[c] * rinv_own;
-      }
-      const double lrm = D[m];  // L[r][m]
-#pragma unroll
-      for (int c = 0; c <= m; ++c) {
-        const double v = gbc(Li[c], m);  // Linv[m][c]
-        if (r > m) acc[c] = fma(-lrm, v, acc[c]);
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-      if (c > r) Li[c] = 0.0;
-    if (act && r < n) {  // packed row r: columns 0..r, zero pad for even r
-      double* row = a.Linv + (start + j) * (size_t)pk + packed_offset_(r);
-      const int len = ((r + 2) >> 1) << 1;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < len) row[c] = (c <= r) ? Li[c] : 0.0;
-    }
-    // ---- Pt1 = X1 Linv^T, Pt2 = Gt Linv^T ----
-    double P1[8], P2[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      double s1 = 0.0, s2 = 0.0;
-#pragma unroll
-      for (int kk = 0; kk <= c; ++kk) {
-        const double v = gbc(Li[kk], c);  // Linv[c][kk]
-        s1 = fma(X[kk], v, s1);
-        s2 = fma(G[kk], v, s2);
-      }
-      P1[c] = s1;
-      P2[c] = s2;
-    }
-    if (act && !last) store_row8(a.Lsub + (start + j) * bs, P1, n, r, true);  // L_{j+1,j}
-    // ---- products with the rows of Pt1 / Pt2, written straight into next step's registers ----
-    //   D_{j+1} = A_{j+1,j+1} - Pt1 Pt1^T, Gt_{j+1} = -Pt2 Pt1^T, S_L += Pt2 Pt2^T;
-    //   last row: S_R = Pt1 Pt1^T and S_sub = -Pt1 Pt2^T go straight to HBM
-    const bool fin = act && last && coupled && r < n;
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      double s11 = 0.0, s21 = 0.0, s22 = 0.0, s12 = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const double v1 = gbc(P1[kk], b);  // Pt1[b][kk]
-        const double v2 = gbc(P2[kk], b);  // Pt2[b][kk]
-        s11 = fma(P1[kk], v1, s11);
-        s21 = fma(P2[kk], v1, s21);
-        s22 = fma(P2[kk], v2, s22);
-        s12 = fma(P1[kk], v2, s12);
-      }
-      D[b] = (b == r && r >= n) ? 1.0 : NA[b] - s11;
-      G[b] = -s21;
-      if (coupled) SL[b] += s22;
-      if (fin && b < n) {
-        a.Sr[(size_t)k * bs + r * n + b] = s11;
-        a.Ssub[(size_t)k * bs + r * n + b] = -s12;
-      }
-    }
-    if (fin) store_row8(a.Sl + (size_t)k * bs, SL, n, r, true);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) X[c] = NX[c];
-  }
-  // failure report (lane 0 of the failing group); no fail when the group never ran
-  if (fail && r == 0 && valid && fail <= n) report_npd(a.err, a.level, fail_j, k, fail);
-}
-
 // ============================================================================================
-// factor_small2_kernel: the same level elimination for n <= 8 with the cross-lane traffic moved
-// from warp shuffles to shared memory.
-//
-// factor_small_kernel broadcasts every operand row with width-8 shuffles: ~470 SHFL per warp-step
-// (a double is two SHFL), and SHFL issues at one warp-instruction per clock per SM -- at cfg3
-// level 0 (1,771 warp-steps per SM) that alone is ~0.4 ms, plus scalar, uncoalesced row loads
-// through the same MIO queue.  Here, per 8-lane group (segment), four 8 x 8 tiles in shared memory
+// factor_small_kernel.  Per 8-lane group (segment), 8 x 8 tiles in shared memory
 // (row stride 10 doubles: the 8 rows of a tile fall in 8 different 16-byte bank quads):
 //   tA  A_{j+1,j+1}, tX  X1 = A_{j+1,j} (or C_R): streamed with cp.async one step ahead, lane r
 //       copies and later reads only its own row r (no cross-lane hazard, no barrier);
@@ -214,9 +60,6 @@ __global__ void __launch_bounds__(kSmallThreads, BTD_FSMALL_MINB) factor_small_k
 //   4. D_{j+1} = A - Pt1 Pt1^T, Gt_{j+1} = -Pt2 Pt1^T, S_L += Pt2 Pt2^T (rows of Pt1 / Pt2 read as
 //      broadcasts); last row: S_R = Pt1 Pt1^T, S_sub = -Pt1 Pt2^T.
 // ~130 shared-memory instructions per warp-step instead of ~470 SHFL + ~60 scalar global accesses.
-// Outputs and NPD coordinates are those of factor_small_kernel (same Y-form algebra; the
-// reference chain permute_split / factorize_btd_batch / solve_btd_batch(F) / compute_schur,
-// bt/schur.py:98-193, bt/block_cholesky.py:24-68).
 // ============================================================================================
 constexpr int kS2LD = 10;                       // padded tile row stride (doubles)
 constexpr int kS2Tile = 8 * kS2LD;              // one 8 x 8 tile
@@ -274,10 +117,7 @@ __device__ __forceinline__ void s2_st_global_row(double* blk, const double (&v)[
   }
 }
 
-#ifndef BTD_S2_MINB
-#define BTD_S2_MINB 4
-#endif
-__global__ void __launch_bounds__(kSmallThreads, BTD_S2_MINB) factor_small2_kernel(FactorArgs a) {
+__global__ void __launch_bounds__(kSmallThreads, 4) factor_small_kernel(FactorArgs a) {
   extern __shared__ __align__(16) double s2sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 3, r = lane & 7;
@@ -289,7 +129,7 @@ __global__ void __launch_bounds__(kSmallThreads, BTD_S2_MINB) factor_small2_kern
   const size_t bs = (size_t)n * n;
   const int pk = packed_offset_(n);
   // CTA-uniform early exit (the CTA's first segment has the lowest k)
-  if (npd_superseded(a.err, a.level, 0, coupled ? a.k0 + blockIdx.x * 16 : 0)) return;
+  if (cta_superseded(a.err, a.level, 0, coupled ? a.k0 + blockIdx.x * 16 : 0)) return;
   const long long start = !valid ? 0 : (coupled ? (long long)a.seps[k] + 1 : 0);
   const long long stop = !valid ? 0 : (coupled ? (long long)a.seps[k + 1] : a.N);
   const int J = (int)(stop - start);
@@ -477,197 +317,9 @@ __global__ void __launch_bounds__(kSmallThreads, BTD_S2_MINB) factor_small2_kern
 }
 
 // ============================================================================================
-// Level solve for n <= 8 (replaces solve_tma_kernel<8> / solve_level_kernel<8>): same step
-// algebra as btd_solve.cuh (down: forward + backward sweep and the fold f_L = C_L^T w_0,
-// f_R = C_R w_last; up: boundary corrections, sweeps, x in the original order; base: one chain),
-// one 8-lane group per segment, DC right-hand-side columns per pass (grid.y covers d).
-// z_j is parked in x (down: scratch; up/base: overwritten by w_j in the backward sweep).
-// ============================================================================================
-// (register caps for more resident CTAs were measured slower: they spill the prefetched operands)
-template <int DC>
-__global__ void __launch_bounds__(kSmallThreads) solve_small_kernel(SolveArgs a) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 3, r = lane & 7;
-  const int n = a.n, d = a.d, mode = a.mode;
-  const int c0 = blockIdx.y * DC;
-  const bool base = mode == kSolveBase;
-  const int k = base ? 0 : (blockIdx.x * 4 + warp) * 4 + g;
-  const bool valid = base ? (blockIdx.x == 0 && warp == 0 && g == 0) : (k < a.K);
-  if (error_raised(a.err)) return;
-  const size_t bs = (size_t)n * n, ps = (size_t)n * d;
-  const int pk = packed_offset_(n);
-  const long long start = !valid ? 0 : (base ? 0 : (long long)a.seps[k] + 1);
-  const long long stop = !valid ? 0 : (base ? a.N : (long long)a.seps[k + 1]);
-  const int J = (int)(stop - start);
-  int jw = J;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) jw = max(jw, __shfl_xor_sync(0xffffffffu, jw, o));
-  const bool rv = valid && r < n;
-  auto ld_vec = [&](const double* p, double (&v)[DC]) {  // row r of an n x d panel, columns c0..
-#pragma unroll
-    for (int c = 0; c < DC; ++c) v[c] = (p && rv && c0 + c < d) ? p[(size_t)r * d + c0 + c] : 0.0;
-  };
-  auto st_vec = [&](double* p, const double (&v)[DC], bool ok) {
-    if (!ok || !rv || !p) return;
-#pragma unroll
-    for (int c = 0; c < DC; ++c)
-      if (c0 + c < d) p[(size_t)r * d + c0 + c] = v[c];
-  };
-  // operand rows of one step, loaded a step ahead of their use (the sweeps are memory-latency
-  // bound: 8-lane groups, a few hundred cycles of shuffles per step against ~1 us of DRAM latency)
-  // L2 priority: the forward sweep's blocks are re-read by the backward sweep (evict_last), which
-  // is their last use (evict_first); thousands of segments are in flight per level
-  const unsigned long long pol_keep = l2_policy_evict_last(), pol_drop = l2_policy_evict_first();
-  auto ld_full = [&](const double* M, bool trans, double (&m8)[8], bool ok) {  // row r of M or M^T
-    const unsigned long long pol = trans ? pol_drop : pol_keep;  // trans <=> backward sweep / fold
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      m8[q] = (ok && rv && q < n) ? ld_hint(trans ? M + (size_t)q * n + r : M + (size_t)r * n + q, pol) : 0.0;
-  };
-  auto ld_pack = [&](const double* P, bool trans, double (&m8)[8], bool ok) {  // row r of Linv or Linv^T
-    const unsigned long long pol = trans ? pol_drop : pol_keep;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const bool in = ok && rv && q < n && (trans ? q >= r : q <= r);
-      m8[q] = in ? ld_hint(trans ? P + packed_offset_(q) + r : P + packed_offset_(r) + q, pol) : 0.0;
-    }
-  };
-  // y (+)= sign * m8 . v  (v broadcast inside the group)
-  auto dot = [&](const double (&m8)[8], const double (&v)[DC], double (&y)[DC], double sign) {
-#pragma unroll
-    for (int c = 0; c < DC; ++c) {
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) s = fma(m8[q], gbc(v[c], q), s);
-      y[c] = fma(sign, s, y[c]);
-    }
-  };
-  auto mv = [&](const double* M, bool trans, const double (&v)[DC], double (&y)[DC], double sign, bool ok) {
-    double m8[8];
-    ld_full(M, trans, m8, ok);
-    dot(m8, v, y, sign);
-  };
-
-  double corr0[DC], corr1[DC], xs0[DC], xs1[DC];
-#pragma unroll
-  for (int c = 0; c < DC; ++c) corr0[c] = corr1[c] = 0.0;
-  if (mode == kSolveUp) {
-    ld_vec(valid ? a.xsep + (size_t)k * ps : nullptr, xs0);
-    ld_vec(valid ? a.xsep + (size_t)(k + 1) * ps : nullptr, xs1);
-    mv(valid ? a.Lsub + (start - 1) * bs : nullptr, false, xs0, corr0, 1.0, valid);  // C_L x_L
-    mv(valid ? a.Lsub + (stop - 1) * bs : nullptr, true, xs1, corr1, 1.0, valid);    // C_R^T x_R
-    st_vec(valid ? a.x + (start - 1) * ps : nullptr, xs0, valid);                    // separator rows
-    st_vec(valid ? a.x + stop * ps : nullptr, xs1, valid && k == a.K - 1);
-  }
-  // ---- forward sweep: z_j = Linv_j (b_j - L_{j,j-1} z_{j-1}) ----
-  double z[DC];
-#pragma unroll
-  for (int c = 0; c < DC; ++c) z[c] = 0.0;
-  double fL[8], fP[8], fb[DC];  // step j's operands (prefetched)
-  auto ld_fwd = [&](int j, double (&L)[8], double (&P)[8], double (&b)[DC]) {
-    const bool act = valid && j < J;
-    const long long row = start + j;
-    ld_full(act && j > 0 ? a.Lsub + (row - 1) * bs : nullptr, false, L, act && j > 0);
-    ld_pack(act ? a.Linv + row * (size_t)pk : nullptr, false, P, act);
-    ld_vec(act ? a.rhs + row * ps : nullptr, b);
-  };
-  ld_fwd(0, fL, fP, fb);
-  for (int j = 0; j < jw; ++j) {
-    const bool act = valid && j < J;
-    const long long row = start + j;
-    double nL[8], nP[8], nb[DC];
-    ld_fwd(j + 1, nL, nP, nb);
-    double t[DC];
-#pragma unroll
-    for (int c = 0; c < DC; ++c) t[c] = fb[c];
-    if (act && j == 0) {
-#pragma unroll
-      for (int c = 0; c < DC; ++c) t[c] -= corr0[c];
-    }
-    if (act && j == J - 1) {
-#pragma unroll
-      for (int c = 0; c < DC; ++c) t[c] -= corr1[c];
-    }
-    dot(fL, z, t, -1.0);  // fL is zero at j == 0
-    double zn[DC];
-#pragma unroll
-    for (int c = 0; c < DC; ++c) zn[c] = 0.0;
-    dot(fP, t, zn, 1.0);
-    if (act) {
-#pragma unroll
-      for (int c = 0; c < DC; ++c) z[c] = zn[c];  // inactive iterations (shorter segments of the warp) keep z
-    }
-    st_vec(act ? a.x + row * ps : nullptr, z, act);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      fL[q] = nL[q];
-      fP[q] = nP[q];
-    }
-#pragma unroll
-    for (int c = 0; c < DC; ++c) fb[c] = nb[c];
-  }
-  // ---- backward sweep: w_j = Linv_j^T (z_j - L_{j+1,j}^T w_{j+1}) ----
-  // group-local index: the groups run their own j = J-1 .. 0 in the same iterations
-  double w[DC], w_last[DC];
-#pragma unroll
-  for (int c = 0; c < DC; ++c) w[c] = w_last[c] = 0.0;
-  auto ld_bwd = [&](int jj, double (&L)[8], double (&P)[8], double (&zz)[DC]) {
-    const int j = jj - (jw - J);
-    const bool act = valid && j >= 0 && jj >= 0;
-    const long long row = start + (act ? j : 0);
-    ld_full(act && j < J - 1 ? a.Lsub + row * bs : nullptr, true, L, act && j < J - 1);
-    ld_pack(act ? a.Linv + row * (size_t)pk : nullptr, true, P, act);
-    ld_vec(act ? a.x + row * ps : nullptr, zz);
-  };
-  __syncwarp();  // this lane's z_j stores (forward) are read back by the same lane only
-  double bL[8], bP[8], bz[DC];
-  ld_bwd(jw - 1, bL, bP, bz);
-  for (int jj = jw - 1; jj >= 0; --jj) {
-    const int j = jj - (jw - J);
-    const bool act = valid && j >= 0;
-    const long long row = start + (act ? j : 0);
-    double nL[8], nP[8], nz[DC];
-    ld_bwd(jj - 1, nL, nP, nz);
-    double t[DC];
-#pragma unroll
-    for (int c = 0; c < DC; ++c) t[c] = bz[c];
-    dot(bL, w, t, -1.0);  // bL is zero at j == J - 1
-    double wn[DC];
-#pragma unroll
-    for (int c = 0; c < DC; ++c) wn[c] = 0.0;
-    dot(bP, t, wn, 1.0);
-    if (act) {
-#pragma unroll
-      for (int c = 0; c < DC; ++c) w[c] = wn[c];
-    }
-    if (mode != kSolveDown) st_vec(act ? a.x + row * ps : nullptr, w, act);
-    if (act && j == J - 1) {
-#pragma unroll
-      for (int c = 0; c < DC; ++c) w_last[c] = w[c];
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      bL[q] = nL[q];
-      bP[q] = nP[q];
-    }
-#pragma unroll
-    for (int c = 0; c < DC; ++c) bz[c] = nz[c];
-  }
-  if (mode == kSolveDown) {  // fold: f_R = C_R w_last ; f_L = C_L^T w_0
-    double fr[DC], fl[DC];
-#pragma unroll
-    for (int c = 0; c < DC; ++c) fr[c] = fl[c] = 0.0;
-    mv(valid ? a.Lsub + (stop - 1) * bs : nullptr, false, w_last, fr, 1.0, valid);
-    mv(valid ? a.Lsub + (start - 1) * bs : nullptr, true, w, fl, 1.0, valid);
-    st_vec(valid ? a.fr + (size_t)k * ps : nullptr, fr, valid);
-    st_vec(valid ? a.fl + (size_t)k * ps : nullptr, fl, valid);
-  }
-}
-
-// ============================================================================================
-// solve_small2_kernel<DC>: the level solve for n <= 8 with shared-memory operand staging (same
-// algebra, outputs and argument contract as solve_small_kernel below; btd_solve.cuh Alg. 5-7 of
-// the reference, bt/schur.py:196-286).  Per step, the group's Lsub block and packed Linv block are
+// solve_small_kernel<DC>: the level solve for n <= 8 (same algebra, outputs and argument contract
+// as solve_level_kernel / solve_tma_kernel, btd_solve.cuh; Alg. 5-7 of the reference,
+// bt/schur.py:196-286).  Per step, the group's Lsub block and packed Linv block are
 // moved into shared memory with coalesced cp.async one step ahead (double-buffered; L2 hints:
 // forward sweep evict_last, backward sweep -- their last use -- evict_first), lane r reads row r
 // (forward) or column r (backward) from the tile, and the two per-step vectors (t, then z / w) are
@@ -709,7 +361,7 @@ __device__ __forceinline__ void ss2_packed(double* tile, const double* blk, int 
 }
 
 template <int DC>
-__global__ void __launch_bounds__(kSmallThreads) solve_small2_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(kSmallThreads) solve_small_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double ss2sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 3, r = lane & 7;

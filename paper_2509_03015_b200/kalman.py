@@ -85,6 +85,9 @@ def _device_array(a: np.ndarray, dev):
 
 #: largest state / dense-measurement dimension of the hand-written assembly kernel (btd_kalman.cuh)
 KERNEL_MAX_DIM = 64
+#: diagonal-block size of the blocked triangular solves of the large-shape path (the seam kernel's
+#: shared-memory limit, btd_seam.cuh kSeamSmemMaxN)
+_TRSM_BLOCK = 128
 
 
 def _raise_first_failure(info_q, info_r):
@@ -103,11 +106,14 @@ def _raise_first_failure(info_q, info_r):
 
 def _build_batched(model: StateSpaceModel, dev):
     """Large shapes (n or dense m > KERNEL_MAX_DIM, e.g. the paper's n = 256, m = 1024 case,
-    PAPER.md:632-641): the same algebra as the reference's per-step loop (kalman.py:99-162) as
-    batched GPU factorizations and products over the horizon (torch.linalg: cuSOLVER / cuBLAS --
-    harness code in front of the factor/solve path, not part of it).  Time-invariant H / Q / R
-    (stride-0 broadcasts) are factored once.  Returns (diag, sub, rhs) on the device."""
+    PAPER.md:632-641): the reference's per-step loop (kalman.py:99-162) batched over the horizon
+    on this package's own seam kernels (btd_seam.cuh, the GPU kernels behind `kernels.py`): the
+    reference calls exactly these primitives -- chol_factor, trsm_lower (twice for an SPD solve)
+    and matrix products -- step by step.  Time-invariant H / Q / R (stride-0 broadcasts) are
+    factored and multiplied once; only elementwise scaling / negation / broadcasting copies run
+    as torch tensor ops.  Returns (diag, sub, rhs) on the device."""
     import torch
+    from . import kernels as kn
     N, n, m = model.horizon, model.state_dim, model.obs_dim
     G, _ = _device_array(model.transition, dev)
     H, _ = _device_array(model.observation, dev)
@@ -115,38 +121,111 @@ def _build_batched(model: StateSpaceModel, dev):
     R, _ = _device_array(model.measurement_cov, dev)
     Z, _ = _device_array(model.observations, dev)
     P, _ = _device_array(model.prior_offsets, dev)
-    # process covariance: Q^{-1}, Q^{-1} G_k, Q^{-1} zeta_k through its Cholesky factor
-    Lq, info_q = torch.linalg.cholesky_ex(Q)
+
+    def over(x, count):  # a (1, ...) broadcast as `count` members (stride-0 view, no copy)
+        return x.expand(count, *x.shape[1:]) if x.shape[0] != count else x
+
+    def chol(x):  # (factor, (first failing member, pivot) or None)
+        f = x.clone()
+        err = kn._ErrWord()
+        kn._chol_dev(kn._Dev(f, True), f.shape[0], f.shape[1], err)
+        rc, st = err.read()
+        if rc == _native.BTD_OK:
+            return f, None
+        if rc != _native.BTD_ERR_NOT_POSITIVE_DEFINITE:
+            kn._check(rc, st)
+        return f, (int(st.member), int(st.pivot))
+
+    def gemm(out, a, b, ta=False, alpha=1.0, beta=0.0):  # out <- alpha op(a) @ b + beta out
+        c = out.shape[0]
+        am = a.shape[2] if ta else a.shape[1]
+        kn._gemm_dev(kn._Dev(out, True), kn._Dev(over(a, c), False), kn._Dev(over(b, c), False), c, am, b.shape[1],
+                     b.shape[2], ta, False, alpha, beta)
+        return out
+
+    def trsm1(f, panel, trans):  # one seam launch: panel <- L^{-1} panel / L^{-T} panel, in place
+        err = kn._ErrWord()
+        kn._trsm_dev(kn._Dev(over(f, panel.shape[0]), False), kn._Dev(panel, True), panel.shape[0], f.shape[1],
+                     panel.shape[2], trans, err)
+        kn._raise_err(err)
+
+    def trsm(f, panel, trans):
+        # blocked substitution over diagonal blocks of <= _TRSM_BLOCK rows (the seam kernel keeps
+        # those in shared memory; larger factors would be read from global memory per FMA), the
+        # off-diagonal coupling as seam GEMM updates (views: no copies)
+        nn = f.shape[1]
+        if nn <= _TRSM_BLOCK:
+            trsm1(f, panel, trans)
+            return panel
+        starts = list(range(0, nn, _TRSM_BLOCK))
+        for i0 in (reversed(starts) if trans else starts):
+            i1 = min(nn, i0 + _TRSM_BLOCK)
+            if not trans and i0 > 0:  # b_i -= L[i, :i] x_{:i}
+                gemm(panel[:, i0:i1], f[:, i0:i1, :i0], panel[:, :i0], alpha=-1.0, beta=1.0)
+            if trans and i1 < nn:  # b_i -= L[i1:, i]^T x_{i1:}
+                gemm(panel[:, i0:i1], f[:, i1:, i0:i1], panel[:, i1:], ta=True, alpha=-1.0, beta=1.0)
+            trsm1(f[:, i0:i1, i0:i1], panel[:, i0:i1], trans)
+        return panel
+
+    def spd_solve(f, panel):  # _chol_solve_spd (kalman.py:99-104)
+        trsm(f, panel, False)
+        trsm(f, panel, True)
+        return panel
+
+
+    # failures in the reference's loop order: process covariance before measurement covariance at
+    # the same step (kalman.py:143-153); a broadcast covariance fails at step 0
+    Lq, fq = chol(Q)
     if model.diagonal_measurement_cov:
         bad = R <= 0.0
-        info_r = torch.where(bad.any(dim=1), bad.to(torch.int64).argmax(dim=1) + 1, 0)
+        rows = torch.nonzero(bad.any(dim=1)).flatten()
+        fr = None
+        if rows.numel():
+            k = int(rows[0])
+            fr = (k, int(bad[k].to(torch.int64).argmax()) + 1)
     else:
-        Lr, info_r = torch.linalg.cholesky_ex(R)
-    info_q = info_q.expand(N) if info_q.shape[0] == 1 else info_q
-    info_r = info_r.expand(N) if info_r.shape[0] == 1 else info_r
-    _raise_first_failure(info_q.cpu(), info_r.cpu())
-    eye = torch.eye(n, dtype=torch.float64, device=dev).expand(Lq.shape[0], n, n).contiguous()
-    q_inv = torch.cholesky_solve(eye, Lq)
-    q_inv_g = torch.cholesky_solve(G, Lq.expand(N, n, n) if Lq.shape[0] == 1 else Lq)
-    q_inv_zeta = torch.cholesky_solve(P.unsqueeze(-1), Lq.expand(N, n, n) if Lq.shape[0] == 1 else Lq)
+        Lr, fr = chol(R)
+    if fq is not None and (fr is None or fq[0] <= fr[0]):
+        raise NotPositiveDefinite(fq[1], block=fq[0], context="process covariance")
+    if fr is not None:
+        raise NotPositiveDefinite(fr[1], block=fr[0], context="measurement covariance")
+
+    nq = Q.shape[0]
+    q_inv = spd_solve(Lq, torch.eye(n, dtype=torch.float64, device=dev).expand(nq, n, n).contiguous())
+    q_inv_g = spd_solve(Lq, G.expand(N, n, n).clone())
+    q_inv_zeta = spd_solve(Lq, over(P, N).reshape(N, n, 1).clone())
     # observation terms H^T R^{-1} H and H^T R^{-1} z (kalman.py:107-127)
     if model.diagonal_measurement_cov:
-        weighted = H / R.unsqueeze(-1)
-        ht_ri_h = H.transpose(1, 2) @ weighted
-        ht_ri_z = H.transpose(1, 2) @ (Z / R).unsqueeze(-1)
+        nb = max(H.shape[0], R.shape[0])
+        white_h = over(H, nb) / over(R, nb).unsqueeze(-1)  # R^{-1} H (elementwise)
+        lhs_h, rhs_h = H, white_h
+        white_z = (over(Z, N) / over(R, N)).unsqueeze(-1)
+        lhs_z = H
     else:
-        white_h = torch.linalg.solve_triangular(Lr, H, upper=False)
-        Lr_n = Lr.expand(N, m, m) if Lr.shape[0] == 1 else Lr
-        white_z = torch.linalg.solve_triangular(Lr_n, Z.unsqueeze(-1), upper=False)
-        ht_ri_h = white_h.transpose(1, 2) @ white_h
-        wh_n = white_h.expand(N, m, n) if white_h.shape[0] == 1 else white_h
-        ht_ri_z = wh_n.transpose(1, 2) @ white_z
-    diag = (q_inv + ht_ri_h).expand(N, n, n).clone()
-    rhs = ht_ri_z.expand(N, n, 1) + G.transpose(1, 2) @ q_inv_zeta
+        nb = max(H.shape[0], R.shape[0])
+        white_h = _white(Lr, H, nb, trsm)
+        lhs_h = rhs_h = white_h
+        white_z = over(Z, N).reshape(N, m, 1).clone()
+        trsm(Lr, white_z, False)
+        lhs_z = white_h
+    # diag_k = Q_k^{-1} + H^T R^{-1} H, computed once over the distinct members
+    nd = max(nq, nb)
+    dsum = over(q_inv, nd).clone()
+    gemm(dsum, over(lhs_h, nd), over(rhs_h, nd), ta=True, beta=1.0)
+    diag = over(dsum, N).clone()
+    rhs = gemm(torch.empty((N, n, 1), dtype=torch.float64, device=dev), over(lhs_z, N), white_z, ta=True)
+    gemm(rhs, G.expand(N, n, n), q_inv_zeta, ta=True, beta=1.0)  # + G_k^T Q_k^{-1} zeta_k
     if N > 1:
-        diag[:-1] += G[1:].transpose(1, 2) @ q_inv_g[1:]
-    sub = -q_inv_g[1:].contiguous()
-    return diag.contiguous(), sub, rhs.contiguous()
+        gemm(diag[:-1], G[1:], q_inv_g[1:], ta=True, beta=1.0)  # + G_{k+1}^T Q^{-1} G_{k+1}
+    sub = torch.neg(q_inv_g[1:])
+    return diag, sub, rhs
+
+
+def _white(Lr, H, nb, trsm):
+    """R^{-1/2} H = L_R^{-1} H over nb members (a fresh copy; H untouched)."""
+    out = (H.expand(nb, *H.shape[1:]) if H.shape[0] != nb else H).clone()
+    trsm(Lr, out, False)
+    return out
 
 
 def build_normal_equations(model: StateSpaceModel, *, device_out: bool = False, _path: str = "auto"):
