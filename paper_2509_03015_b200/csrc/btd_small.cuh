@@ -117,7 +117,10 @@ __device__ __forceinline__ void s2_st_global_row(double* blk, const double (&v)[
   }
 }
 
-__global__ void __launch_bounds__(kSmallThreads, 4) factor_small_kernel(FactorArgs a) {
+#ifndef BTD_S2_MINB
+#define BTD_S2_MINB 4
+#endif
+__global__ void __launch_bounds__(kSmallThreads, BTD_S2_MINB) factor_small_kernel(FactorArgs a) {
   extern __shared__ __align__(16) double s2sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 3, r = lane & 7;
@@ -173,11 +176,24 @@ __global__ void __launch_bounds__(kSmallThreads, 4) factor_small_kernel(FactorAr
   }
   if (valid && coupled) {
     load_col8(G, a.sub + (start - 1) * bs, n, r, true);
-    double t[8];
-    load_row8(t, a.sub + (start - 1) * bs, n, r, true, false);
-    store_row8(a.Lsub + (start - 1) * bs, t, n, r, true);
-    load_row8(t, a.sub + (stop - 1) * bs, n, r, true, false);
-    store_row8(a.Lsub + (stop - 1) * bs, t, n, r, true);
+    // the hierarchy's copies of C_L and C_R (two contiguous blocks: 16-byte copies for even n)
+    if ((n & 1) == 0) {
+      const int nc = n * n / 2;
+      const double2* cl = reinterpret_cast<const double2*>(a.sub + (start - 1) * bs);
+      const double2* cr = reinterpret_cast<const double2*>(a.sub + (stop - 1) * bs);
+      double2* dl = reinterpret_cast<double2*>(a.Lsub + (start - 1) * bs);
+      double2* dr = reinterpret_cast<double2*>(a.Lsub + (stop - 1) * bs);
+      for (int c = r; c < nc; c += 8) {
+        dl[c] = cl[c];
+        dr[c] = cr[c];
+      }
+    } else {
+      double t[8];
+      load_row8(t, a.sub + (start - 1) * bs, n, r, true, false);
+      store_row8(a.Lsub + (start - 1) * bs, t, n, r, true);
+      load_row8(t, a.sub + (stop - 1) * bs, n, r, true, false);
+      store_row8(a.Lsub + (stop - 1) * bs, t, n, r, true);
+    }
   } else {
 #pragma unroll
     for (int c = 0; c < 8; ++c) G[c] = 0.0;
