@@ -84,10 +84,6 @@ struct FactorShape {
   static_assert(NWB == 0 || 16 * NWB == NT, "group B owns 16 rows of the fill block per warp");
 };
 
-#ifndef BTD_RCP_CHAIN
-#define BTD_RCP_CHAIN true
-#endif
-
 constexpr int kBarA = 1;  // named barrier of group A
 constexpr int kBarB = 2;  // named barrier of group B
 
@@ -231,17 +227,11 @@ __device__ __forceinline__ int panel_chain(double* DL, int p0, int lane) {
 // shared-memory wavefronts of two 8-byte accesses on the LD = NT + 4 layout.
 template <int LD>
 __device__ __forceinline__ void sub_frag(double* DL, int tr, int tc, int lane, const double (&acc)[2]) {
-#ifdef BTD_SCALAR_FRAG
-  double* dst = DL + (tr * 8 + (lane >> 2)) * LD + tc * 8 + 2 * (lane & 3);
-  dst[0] -= acc[0];
-  dst[1] -= acc[1];
-#else
   double2* dst = reinterpret_cast<double2*>(DL + (tr * 8 + (lane >> 2)) * LD + tc * 8 + 2 * (lane & 3));
   double2 v = *dst;
   v.x -= acc[0];
   v.y -= acc[1];
   *dst = v;
-#endif
 }
 
 // rank-8 update of one 8x8 tile (tr, tc) by panel p: A[tr][tc] -= L[tr][p] L[tc][p]^T
@@ -387,8 +377,8 @@ __device__ int potrf_trtri(double* DL, int* s_fail, unsigned long long* leaf_bar
   for (int p = 0; p < NP; ++p) {
     const int p0 = p * 8;
     if (warp == 0) {
-      const int f = (p0 + 32 < NT) ? panel_chain<NT, true, BTD_RCP_CHAIN>(DL, p0, lane)
-                                   : panel_chain<NT, false, BTD_RCP_CHAIN>(DL, p0, lane);
+      const int f = (p0 + 32 < NT) ? panel_chain<NT, true, true>(DL, p0, lane)
+                                   : panel_chain<NT, false, true>(DL, p0, lane);
       if (lane == 0) *s_fail = f;
       BTD_PHASE(6);
     } else if (p > 0) {
@@ -625,11 +615,7 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
     const bool last = (j == J - 1);
     // ================= phase 1: A factors D_j ; B finishes step j-1 =================
     int fail = 0;
-#ifdef BTD_R1_CHAIN
-    constexpr bool kChain = false;  // A/B builds: the round-1 four-warp potrf_trtri
-#else
     constexpr bool kChain = NT >= 32;
-#endif
     if constexpr (kChain) {
       // single-warp left-looking pivot chain (btd_chain.cuh), then the inverse by recursive
       // doubling on the whole of group A
@@ -706,7 +692,6 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
       cp_async_commit();
     }
     // D_{j+1} = A_{j+1,j+1} - P1^T P1  (or S_R at the last row of a coupled segment)
-#ifndef BTD_D16
     if constexpr (NT == 64) {
       // 36 lower 8x8 tiles balanced over the 8 warps (4-5 each, max 5 DMMAs per k step instead of
       // 8 for the warps that held two 16x16 tiles): warps 2p, 2p+1 share the tile rows 7-p and p,
@@ -753,7 +738,6 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
       BTD_PHASE(3);
       continue;
     }
-#endif
     double acc[S::MAXD][SUB][SUB][2];
     int drr[S::MAXD], dcc[S::MAXD];
 #pragma unroll

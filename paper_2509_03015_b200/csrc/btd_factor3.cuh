@@ -197,12 +197,8 @@ __global__ void __launch_bounds__(StreamShape::NTHREADS, 1) factor_stream_kernel
     const long long tstep = clock64();
     if (in_a) {
       // ======== group A: Cholesky of D_j, leaves published one by one ========
-#ifdef BTD_R1_CHAIN
-      const int fail = potrf_trtri<NT, false>(DL, &s_fail_a, leaf_bar);
-#else
       // single-warp left-looking chain (btd_chain.cuh): no group barriers on the critical path
       const int fail = warp == 0 ? chain_potrf64<LD, NT>(DL, lane, leaf_bar) : 0;
-#endif
       if (fail && tid == 0) s_fail = fail;
       if (tid == 0) BTD_SPROF(11, tstep);
     } else {

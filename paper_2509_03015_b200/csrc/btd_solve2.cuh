@@ -246,16 +246,12 @@ __device__ __forceinline__ void mv64(const double* __restrict__ M, const double*
 
 template <int NT, int DC>
 __device__ __forceinline__ void mv_full_rows(const double* M, const double* x, double (&s)[DC]) {
-#ifndef BTD_SOLVE_ROTATED
   if constexpr (NT == 64) { mv64<DC, false>(M, x, s); return; }
-#endif
   mv_rows<NT, DC>(M, x, s);
 }
 template <int NT, int DC>
 __device__ __forceinline__ void mv_packed_rows(const double* M, const double* x, double (&s)[DC]) {
-#ifndef BTD_SOLVE_ROTATED
   if constexpr (NT == 64) { mv64<DC, true>(M, x, s); return; }
-#endif
   mv_pack_rows<NT, DC>(M, x, s);
 }
 
@@ -339,9 +335,7 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
     if (lane == 0) {
       int slot = 0;
       unsigned phase = 0;
-#ifndef BTD_SOLVE_NOHINT
       const unsigned long long pol_keep = l2_policy_evict_last(), pol_drop = l2_policy_evict_first();
-#endif
       constexpr unsigned fb = NT * NT * sizeof(double), pb = S::PACK * sizeof(double);
       const unsigned vb = (unsigned)(n * d * sizeof(double));
       SegBounds sb(a, mode, blockIdx.x, K);
@@ -372,20 +366,12 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
           if (!vec_bulk) vec = nullptr;
           mbar_wait(&empty_bar[slot], phase ^ 1);
           double* st = ring + slot * STAGE;
-#ifdef BTD_SOLVE_NOLOAD  // diagnostic: consumers run on stale slot contents (pure consumer time)
-          full = pack = vec = nullptr;
-#endif
           mbar_arrive_expect_tx(&full_bar[slot], (full ? fb : 0) + (pack ? pb : 0) + (vec ? vb : 0));
-#ifndef BTD_SOLVE_NOHINT
           // forward-sweep blocks are read again by the backward sweep: keep them in L2 (evict_last);
           // the backward sweep is their last use (evict_first)
           const unsigned long long pol = (kind == kStepF) ? pol_keep : pol_drop;
           if (full) tma_load_1d_hint(st, full, fb, &full_bar[slot], pol);
           if (pack) tma_load_1d_hint(st + S::FULL, pack, pb, &full_bar[slot], pol);
-#else
-          if (full) tma_load_1d(st, full, fb, &full_bar[slot]);
-          if (pack) tma_load_1d(st + S::FULL, pack, pb, &full_bar[slot]);
-#endif
           if (vec) tma_load_1d(st + S::FULL + S::PACK, vec, vb, &full_bar[slot]);
           if (++slot == STAGES) {
             slot = 0;
@@ -427,9 +413,6 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
       BTD_SPH(0);
       mbar_wait(&full_bar[slot], phase);
       BTD_SPH(1);
-#ifdef BTD_SOLVE_NOMATH  // diagnostic: consumers only release the slots (pure producer/memory time)
-      kind = kStepNone;
-#endif
       const double* sf = ring + slot * STAGE;
       const double* sp = sf + S::FULL;
       const double* sv = sp + S::PACK;
