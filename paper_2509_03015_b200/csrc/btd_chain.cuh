@@ -103,6 +103,7 @@ __device__ __forceinline__ int chain_potrf(double* DL, int lane, unsigned long l
       }
     }
     // ---- 4. leaf: lane c < 8 computes column c of L_pp^{-1} ----
+    __syncwarp();  // every lane has read the diagonal tile (step 2) before lanes 0-7 overwrite it
     if (lane < 8) {
       const int c = lane;
       double x[8];

@@ -6,7 +6,8 @@ import torch
 import paper_2509_03015_b200 as pkg
 from paper_2509_03015_b200 import _native
 
-cases = [(40, 8, 2, 8, 4), (60, 32, 1, 8, 4), (300, 64, 1, 64, 8), (600, 64, 1, 8, 8),  # small / level / stream / 2-CTA solve
+cases = [(40, 8, 2, 8, 4), (200, 8, 1, 8, 8), (150, 5, 4, 8, 8), (90, 6, 2, 8, 3),  # n <= 8: small kernels (DC 1/2/4, odd n)
+          (60, 32, 1, 8, 4), (300, 64, 1, 64, 8), (600, 64, 1, 8, 8),  # small / level / stream / 2-CTA solve
          (80, 128, 2, 8, 4), (700, 128, 1, 64, 8), (30, 100, 1, 8, 4), (20, 256, 3, 4, 3)]  # tiled, wide solve, padded
 for N, n, d, cross, rho in cases:
     A, B = pkg.generate_spd_btd(N, n, d, seed=1)
