@@ -432,8 +432,8 @@ __global__ void __launch_bounds__(BTHREADS) big_potrf_kernel(BigPotrfArgs g) {
       }
     }
     csync();
-    if (C > 1) {  // every rank learns the outcome from rank 0's shared memory
-      if (tid == 0) {
+    if (C > 1) {  // every other rank learns the outcome from rank 0's shared memory
+      if (tid == 0 && rank != 0) {
         unsigned addr = (unsigned)__cvta_generic_to_shared(&s_fail), remote;
         asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(addr));
         int f;

@@ -16,11 +16,16 @@
 
 namespace btd {
 
-// leaf_bars (optional): panel p's mbarrier is arrived on once its leaf and the rows below it are in
-// shared memory (a streaming consumer may start that column block of its triangular solve); on a
+// leaf_bar0 (optional, > 0): panel p's leaf and the rows below it are published on the named
+// barrier leaf_bar0 + p (bar.arrive by this warp, `leaf_count` threads in total with the consumers'
+// bar.sync): a streaming consumer may start that column block of its triangular solve.  On a
 // failure every remaining barrier is arrived on so no consumer waits forever.
+__device__ __forceinline__ void named_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 template <int LD, int NT>
-__device__ __forceinline__ int chain_potrf(double* DL, int lane, unsigned long long* leaf_bars = nullptr) {
+__device__ __forceinline__ int chain_potrf(double* DL, int lane, int leaf_bar0 = 0, int leaf_count = 0) {
   static_assert(NT == 32 || NT == 64, "chain_potrf factors 32 x 32 or 64 x 64 tiles");
   constexpr int NP = NT / 8;
   int fail = 0;
@@ -68,8 +73,8 @@ __device__ __forceinline__ int chain_potrf(double* DL, int lane, unsigned long l
           if (!(i == k + 1 && j == k + 1)) a[i][j] = fma(-t[i], a[j][k], a[i][j]);
     }
     if (fail) {  // uniform over the warp (every lane factored the same tile)
-      if (leaf_bars && lane == 0)
-        for (int q = p; q < NP; ++q) mbar_arrive(&leaf_bars[q]);
+      if (leaf_bar0)
+        for (int q = p; q < NP; ++q) named_arrive(leaf_bar0 + q, leaf_count);
       return fail;
     }
     double lt[8][8];  // L_pp (normalized)
@@ -126,17 +131,14 @@ __device__ __forceinline__ int chain_potrf(double* DL, int lane, unsigned long l
       DL[(p0 + c) * LD + NT] = rinv[c];
     }
     __syncwarp();
-    if (leaf_bars && lane == 0) {
-      __threadfence_block();
-      mbar_arrive(&leaf_bars[p]);
-    }
+    if (leaf_bar0) named_arrive(leaf_bar0 + p, leaf_count);
   }
   return 0;
 }
 
 template <int LD, int NT>
-__device__ __forceinline__ int chain_potrf64(double* DL, int lane, unsigned long long* leaf_bars = nullptr) {
-  return chain_potrf<LD, NT>(DL, lane, leaf_bars);
+__device__ __forceinline__ int chain_potrf64(double* DL, int lane, int leaf_bar0 = 0, int leaf_count = 0) {
+  return chain_potrf<LD, NT>(DL, lane, leaf_bar0, leaf_count);
 }
 
 }  // namespace btd

@@ -248,6 +248,9 @@ def test_host_input_npd_coordinates_match_device_path():
     (3000, 128, 8, 64, [(9 * 3 + 1 + 2, 100), (9 * 5 + 1 + 2, 5)]),
     # ... and an earlier step in the second half-level stream beats a later step in the first
     (3000, 128, 8, 64, [(9 * 3 + 1 + 4, 5), (9 * 200 + 1 + 1, 70)]),
+    # a level-0 separator that fails in the serial base (cluster-resident base kernel, n = 128, 256)
+    (70, 128, 8, 64, [(9 * 3, 5)]),
+    (70, 256, 8, 64, [(9 * 4, 200), (9 * 6, 3)]),
 ])
 def test_npd_coordinates_every_kernel_vs_oracle(N, n, rho, cross, bad):
     """A non-positive pivot reports the oracle's (pivot, level, member, block) -- the reference's
