@@ -5,9 +5,11 @@
 // bt/block_cholesky.py:24-68); the schedule removes the triangular inverse and the Pt product from
 // the per-step critical path:
 //
-//   group A (warps 0-3)  : Cholesky of D_j, panel by panel (potrf_trtri<64, false>): L with its
-//                          8x8 diagonal tiles inverted ("leaves"); every leaf is published on an
-//                          mbarrier as soon as it exists.
+//   group A (warp 0)     : Cholesky of D_j, panel by panel (single-warp chain, btd_chain.cuh): L
+//                          with its 8x8 diagonal tiles inverted ("leaves"); every leaf is published
+//                          on its own named barrier (bar.arrive; group B waits with bar.sync) as
+//                          soon as it exists.  (Round 1 used mbarriers, which compute-sanitizer's
+//                          racecheck does not model; with named barriers racecheck checks it.)
 //   group B (warps 4-15) : owns 24 register-resident 8-row tiles of the stacked right-hand side
 //                          [X1; Gt; I] (X1 = A_{j+1,j} or C_R, Gt = fill coupling, I = identity)
 //                          and runs the blocked triangular solve Pt = [X1; Gt; I] L_j^{-T} one
@@ -49,7 +51,8 @@ struct StreamShape {
   static_assert(NWA == 4, "potrf group is 4 warps at NT = 64");
 };
 
-constexpr int kBarS = 3;  // named barrier of group B (streaming kernel)
+constexpr int kBarS = 3;      // named barrier of group B (streaming kernel)
+constexpr int kBarLeaf0 = 4;  // named barriers 4..11: leaf p published by the pivot chain (warp 0) to group B
 
 // cp.async staging of an n x n row-major block into an NT x LD tile by `nb` threads (index gt).
 template <int NT, int LD>
@@ -153,7 +156,6 @@ __global__ void __launch_bounds__(StreamShape::NTHREADS, 1) factor_stream_kernel
   double* XP = smem;                // rows 0..63: Pt1, rows 64..127: Pt2 (of the last finished step)
   double* DL = smem + 2 * NT * LD;  // D_j -> L_j (+ leaves)
   double* DN = DL + NT * LD;        // A_{j+1,j+1} (prefetch)
-  __shared__ __align__(8) unsigned long long leaf_bar[8];
   __shared__ int s_fail_a, s_fail;
 
   const int k = args.k0 + blockIdx.x;
@@ -165,7 +167,42 @@ __global__ void __launch_bounds__(StreamShape::NTHREADS, 1) factor_stream_kernel
   const int n = args.n;
   const size_t bs = (size_t)n * n;
   const int pk = packed_offset_(n);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, hw = tid >> 5;
+  // Roles by SM sub-partition: group A is warp 0 (the pivot chain) plus the warps that share its
+  // sub-partition (read from %warpid), so none of group B's DMMA work is issued next to the chain
+  // (a DMMA warp on the chain's sub-partition slows it ~1.6x; tools/chain2_bench.cu).  `warp` is
+  // the logical warp index every role below is keyed on; logical warp 0 is hardware warp 0.
+  __shared__ int s_smsp[SS::NW];
+  {
+    unsigned wid;
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+    if (lane == 0) s_smsp[hw] = (int)(wid & 3);
+  }
+  __syncthreads();
+  int warp = 0;
+  {
+    const int a0 = s_smsp[0];
+    bool inA[SS::NW];
+    int na = 0;
+#pragma unroll
+    for (int w = 0; w < SS::NW; ++w) {
+      inA[w] = (w == 0) || (s_smsp[w] == a0 && na < NWA);
+      na += inA[w];
+    }
+#pragma unroll
+    for (int w = 1; w < SS::NW; ++w)  // an unexpected warp placement: fill group A in order
+      if (!inA[w] && na < NWA) {
+        inA[w] = true;
+        ++na;
+      }
+    int pos = 0;
+#pragma unroll
+    for (int w = 0; w < SS::NW; ++w)
+      if (inA[w]) warp = (w == hw) ? pos++ : (pos++, warp);
+#pragma unroll
+    for (int w = 0; w < SS::NW; ++w)
+      if (!inA[w]) warp = (w == hw) ? pos++ : (pos++, warp);
+  }
   const bool in_a = warp < NWA;
   const int b = warp - NWA;  // group-B warp index
   double* sl = coupled ? args.Sl + (size_t)k * bs : nullptr;
@@ -174,8 +211,6 @@ __global__ void __launch_bounds__(StreamShape::NTHREADS, 1) factor_stream_kernel
 
   // ---- prologue ----
   if (tid == 0) {
-    for (int q = 0; q < 8; ++q) mbar_init(&leaf_bar[q], 1);
-    fence_barrier_init();
     s_fail = 0;
   }
   stage_block_async_part<NT, LD>(DL, args.diag + start * bs, n, tid, SS::NTHREADS);
@@ -193,12 +228,11 @@ __global__ void __launch_bounds__(StreamShape::NTHREADS, 1) factor_stream_kernel
 
   for (int j = 0; j < J; ++j) {
     const bool last = (j == J - 1);
-    const unsigned par = (unsigned)(j & 1);
     const long long tstep = clock64();
     if (in_a) {
       // ======== group A: Cholesky of D_j, leaves published one by one ========
       // single-warp left-looking chain (btd_chain.cuh): no group barriers on the critical path
-      const int fail = warp == 0 ? chain_potrf64<LD, NT>(DL, lane, leaf_bar) : 0;
+      const int fail = warp == 0 ? chain_potrf64<LD, NT>(DL, lane, kBarLeaf0, 32 + NB) : 0;
       if (fail && tid == 0) s_fail = fail;
       if (tid == 0) BTD_SPROF(11, tstep);
     } else {
@@ -233,7 +267,7 @@ __global__ void __launch_bounds__(StreamShape::NTHREADS, 1) factor_stream_kernel
       // ---- blocked triangular solve [X; G; Y] L_j^{-T}, one column block behind the pivot chain ----
 #pragma unroll
       for (int p = 0; p < 8; ++p) {
-        mbar_wait(&leaf_bar[p], par);
+        named_sync(kBarLeaf0 + p, 32 + NB);  // leaf p and the rows below it (chain_potrf)
         const double* lp = DL + (8 * p + (lane >> 2)) * LD + 8 * p + (lane & 3);
         const double lb0 = lp[0], lb1 = lp[4];  // B = Linv_pp^T
         const bool actY = p >= b;  // the identity tile is zero left of its diagonal block
