@@ -570,6 +570,32 @@ __device__ __forceinline__ void sl_update(const double* XP, double* sl, int n, b
   }
 }
 
+// Logical warp index of hardware warp `hw` for factor_level_kernel<64> (see there).  Reads
+// %warpid: hardware warp slot on the SM, sub-partition = slot % 4.
+template <int NW, int NWA>
+__device__ __forceinline__ int level_warp_roles(int hw, int lane) {
+  __shared__ int s_wid[NW];
+  unsigned wid;
+  asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+  if (lane == 0) s_wid[hw] = (int)wid;
+  __syncthreads();
+  int lo = s_wid[0];
+#pragma unroll
+  for (int w = 1; w < NW; ++w) lo = min(lo, s_wid[w]);
+  const int sc = (lo / NW) & 1, so = sc ^ 1;  // this CTA's chain sub-partition, the other CTA's
+  // order: warps on sc, then on so, then the rest (hardware order within a class); the position
+  // in that order is the logical index (group A = the first NWA, the chain = the first)
+  auto key = [&](int w) {
+    const int sp = s_wid[w] & 3;
+    return ((sp == sc ? 0 : sp == so ? 1 : 2) << 8) | w;
+  };
+  const int mk = key(hw);
+  int mine = 0;
+#pragma unroll
+  for (int v = 0; v < NW; ++v) mine += key(v) < mk;
+  return mine;
+}
+
 template <int NT>
 __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MINB)
     factor_level_kernel(FactorArgs args) {
@@ -589,7 +615,13 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
   const int J = (int)(stop - start);
   const int n = args.n;
   const size_t bs = (size_t)n * n;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
+  // Logical warp roles by SM sub-partition (NT = 64, two CTAs per SM): the pivot chain (logical
+  // warp 0) runs on sub-partition `sc` (0 or 1 by the CTA's warp slots on the SM, so the two
+  // resident CTAs' chains sit on different sub-partitions), the rest of group A are this CTA's
+  // warps on the two chain sub-partitions, and group B -- the DMMA work that runs concurrently
+  // with the chains -- are its warps on the other two.  Every role below is keyed on `warp`.
+  const int warp = NT == 64 ? level_warp_roles<NW, NWA>(tid >> 5, lane) : tid >> 5;
   const bool in_a = warp < NWA;
   const int wb = warp - NWA;  // warp index inside group B
   double* sl = args.Sl + (size_t)k * bs;
@@ -635,7 +667,7 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
     constexpr int SKIPB = 0;
     if (j > 0 && (NWB == 0 || (!in_a && wb >= SKIPB))) {
       const int w = NWB ? wb - SKIPB : 0, nw = NWB ? NWB - SKIPB : 1, nb = NWB ? (NWB - SKIPB) * 32 : 32;
-      const int gt = NWB ? tid - (NWA + SKIPB) * 32 : tid;
+      const int gt = NWB ? (warp - NWA - SKIPB) * 32 + lane : tid;
       if (coupled) {
         sl_update<NT>(XP, sl, n, j == 1, w, nw, lane);
         named_sync(kBarB, nb);
@@ -671,7 +703,7 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
         cp_async_commit();
       }
     }
-    if (in_a && tid == 0) s_fail = fail;
+    if (warp == 0 && lane == 0) s_fail = fail;  // logical warp 0 (the chain) is in group A
     __syncthreads();
     BTD_PHASE(1);
     if (s_fail) {
