@@ -633,11 +633,14 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
   else if (coupled)
     stage_block_async<NT, LD, NTHREADS>(XP, args.sub + (stop - 1) * bs, n);
   cp_async_commit();
-  if (coupled) {
-    stage_block_transposed<NT, LD, NTHREADS>(XP + NT * LD, args.sub + (start - 1) * bs, n);
-    copy_block<NTHREADS>(args.Lsub + (start - 1) * bs, args.sub + (start - 1) * bs, n);  // C_L
-    copy_block<NTHREADS>(args.Lsub + (stop - 1) * bs, args.sub + (stop - 1) * bs, n);    // C_R
-  }
+  // Gt_0 = C_L^T and the hierarchy's copies of C_L, C_R: needed only from phase 2 of step 0, so
+  // group B does them while the first pivot chain runs (single-warp CTAs: here)
+  auto coupling_work = [&](int t, int nt) {
+    stage_block_transposed_part<NT, LD>(XP + NT * LD, args.sub + (start - 1) * bs, n, t, nt);
+    copy_block_part(args.Lsub + (start - 1) * bs, args.sub + (start - 1) * bs, n, t, nt);  // C_L
+    copy_block_part(args.Lsub + (stop - 1) * bs, args.sub + (stop - 1) * bs, n, t, nt);    // C_R
+  };
+  if (coupled && NWB == 0) coupling_work(tid, NTHREADS);
   cp_async_wait_all();
   for (int r = n + tid; r < NT; r += NTHREADS) DL[r * LD + r] = 1.0;
   __syncthreads();
@@ -665,6 +668,7 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
     }
     if (NWB == 0) __syncthreads();  // single-warp CTA: group B work runs after the factor
     constexpr int SKIPB = 0;
+    if (j == 0 && coupled && NWB > 0 && !in_a) coupling_work((warp - NWA) * 32 + lane, NWB * 32);
     if (j > 0 && (NWB == 0 || (!in_a && wb >= SKIPB))) {
       const int w = NWB ? wb - SKIPB : 0, nw = NWB ? NWB - SKIPB : 1, nb = NWB ? (NWB - SKIPB) * 32 : 32;
       const int gt = NWB ? (warp - NWA - SKIPB) * 32 + lane : tid;
