@@ -289,12 +289,12 @@ __device__ __forceinline__ void tile_update_tri(double* DL, int off, int m, int 
 // Recursive doubling on DMMA, run by the NWA warps of group A (named barrier kBarA), turning
 // L with inverted 8x8 diagonal tiles into the full inverse Linv, in place:
 //   [[A,0],[B,C]]^{-1} = [[Ai,0],[-Ci B Ai, Ci]]   for blocks of 8, 16, 32 rows.
-template <int NT>
+template <int NT, int NWT = FactorShape<NT>::NWA>
 __device__ __forceinline__ void trtri_doubling(double* DL, int warp, int lane) {
   using S = FactorShape<NT>;
   constexpr int LD = S::LD;
-  constexpr int NWA = S::NWA;
-  constexpr int MAXV = S::MAXV;
+  constexpr int NWA = NWT;  // warps running the inverse (named barrier kBarA over them)
+  constexpr int MAXV = (NT * NT / 256 + NWA - 1) / NWA > 0 ? (NT * NT / 256 + NWA - 1) / NWA : 1;
 
   // ---- recursive doubling: [[A,0],[B,C]]^{-1} = [[Ai,0],[-Ci B Ai, Ci]] on DMMA ----
 #pragma unroll
@@ -661,7 +661,18 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
         }
         named_sync(kBarA, NWA * 32);
         fail = s_fail_a;
+#ifdef BTD_TRTRI2
+        // A/B: the inverse on the chain's sub-partition only (logical warps 0, 1)
+        if (NT == 64) {
+          if (!fail && warp < 2) {
+            trtri_doubling<NT, 2>(DL, warp, lane);
+          }
+        } else if (!fail) {
+          trtri_doubling<NT>(DL, warp, lane);
+        }
+#else
         if (!fail) trtri_doubling<NT>(DL, warp, lane);
+#endif
       }
     } else {
       if (in_a) fail = potrf_trtri<NT>(DL, &s_fail);
