@@ -661,18 +661,7 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
         }
         named_sync(kBarA, NWA * 32);
         fail = s_fail_a;
-#ifdef BTD_TRTRI2
-        // A/B: the inverse on the chain's sub-partition only (logical warps 0, 1)
-        if (NT == 64) {
-          if (!fail && warp < 2) {
-            trtri_doubling<NT, 2>(DL, warp, lane);
-          }
-        } else if (!fail) {
-          trtri_doubling<NT>(DL, warp, lane);
-        }
-#else
         if (!fail) trtri_doubling<NT>(DL, warp, lane);
-#endif
       }
     } else {
       if (in_a) fail = potrf_trtri<NT>(DL, &s_fail);
