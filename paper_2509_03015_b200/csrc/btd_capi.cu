@@ -215,6 +215,22 @@ unsigned flat_grid(int64_t elements) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 16));
 }
 
+// Next-level diagonal blocks (btd_factor.cuh): a warp per block row for even n >= 32 (cfg2 level 0
+// 131 -> 106 us); the flat element kernel for small blocks (a warp per 8-double row idles 28 lanes:
+// cfg3 level 0 40 -> 187 us).
+void launch_assemble(const double* diag, const int* seps, double* next_diag, const double* Sr, int K, int64_t n,
+                     btd::DevErr* err, cudaStream_t s) {
+  const int64_t P = (int64_t)K + 1;
+  if ((n & 1) == 0 && n >= 32) {
+    const int64_t warps = P * n;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)device_sms() * 16));
+    btd::assemble_schur_diag_rows_kernel<<<grid, 256, 0, s>>>(diag, seps, next_diag, Sr, K, (int)n, err);
+  } else {
+    btd::assemble_schur_diag_kernel<<<flat_grid(P * n * n), 256, 0, s>>>(diag, seps, next_diag, Sr, K, (int)n, err);
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
 int pick_nt(int64_t n) {
   if (n <= 8) return 8;
   if (n <= 16) return 16;
@@ -1288,8 +1304,8 @@ static int enqueue_factor(btd_hierarchy* h, const double* diag, const double* su
       }
       prof_mark(h, stream);
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(big level)");
-      btd::assemble_schur_diag_kernel<<<flat_grid(lp.P * h->n * h->n), 256, 0, stream>>>(
-          cd, (const int*)(pers + lp.off_seps), next_diag, (const double*)(scr + lp.off_sr), (int)lp.K, n, err); g_launches.fetch_add(1, std::memory_order_relaxed);
+      launch_assemble(cd, (const int*)(pers + lp.off_seps), next_diag, (const double*)(scr + lp.off_sr), (int)lp.K, n,
+                      err, stream);
       e = cudaGetLastError();
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(assemble)");
       cd = next_diag;
@@ -1340,7 +1356,7 @@ static int enqueue_factor(btd_hierarchy* h, const double* diag, const double* su
       prof_mark(h, stream);
       if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(level kernel)");
     }
-    btd::assemble_schur_diag_kernel<<<flat_grid(lp.P * h->n * h->n), 256, 0, stream>>>(cd, a.seps, a.Sl, a.Sr, (int)lp.K, n, err); g_launches.fetch_add(1, std::memory_order_relaxed);
+    launch_assemble(cd, a.seps, a.Sl, a.Sr, (int)lp.K, n, err, stream);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(assemble)");
     cd = a.Sl;

@@ -848,6 +848,38 @@ __global__ void assemble_schur_diag_kernel(const double* diag, const int* seps, 
   }
 }
 
+// The same for even n, a warp per block row: 16-byte accesses over the row's lower part (columns
+// 0..r, plus the pair partner of column r, which lands in the never-read upper triangle), no
+// per-element index division.
+__global__ void assemble_schur_diag_rows_kernel(const double* diag, const int* seps, double* next_diag,
+                                                const double* Sr, int K, int n, const DevErr* err) {
+  if (error_raised(err)) return;
+  const long long rows = (long long)(K + 1) * n;
+  const int lane = threadIdx.x & 31;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const size_t bs = (size_t)n * n;
+  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < rows; w += nw) {
+    const int p = (int)(w / n), r = (int)(w % n);
+    const double* a = diag + (size_t)seps[p] * bs + (size_t)r * n;
+    double* o = next_diag + (size_t)p * bs + (size_t)r * n;
+    const double* sr = Sr + ((size_t)p - 1) * bs + (size_t)r * n;
+    for (int c = 2 * lane; c <= r; c += 64) {
+      double2 v = *reinterpret_cast<const double2*>(a + c);
+      if (p < K) {
+        const double2 t = *reinterpret_cast<const double2*>(o + c);
+        v.x -= t.x;
+        v.y -= t.y;
+      }
+      if (p > 0) {
+        const double2 t = *reinterpret_cast<const double2*>(sr + c);
+        v.x -= t.x;
+        v.y -= t.y;
+      }
+      *reinterpret_cast<double2*>(o + c) = v;
+    }
+  }
+}
+
 // Upper triangle of every n x n block := its lower triangle (debug export of Schur diagonals).
 __global__ void mirror_lower_kernel(double* blocks, long long P, int n) {
   const size_t bs = (size_t)n * n, total = (size_t)P * bs;
