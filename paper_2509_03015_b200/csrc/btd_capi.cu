@@ -731,7 +731,12 @@ cudaError_t big_factor_level(const BigCtx& c, int level, int Jmax, int n, const 
 // per segment streaming the blocks, instead of tile GEMMs that would fill d of 64 output columns.
 // Narrow levels and the serial base keep the GEMM path (one CTA per segment would stream whole
 // blocks through a single SM).
+// 5 <= d <= 8: solve_dmma_kernel (btd_solve3.cuh), one CTA per segment, the block products on
+// DMMA with the matrix fragments read from global memory ((512, 128, 8): solve 4.63 -> 3.28 ms).
+// Wider right-hand sides keep the tile GEMMs: with one CTA per 8-column slice every slice re-reads
+// the blocks (cfg4, d = 64: 15.2 -> 34 ms measured).
 bool use_wide_solve(int n, int d, int64_t K) {
+  if (d >= 5 && d <= 8 && n % 64 == 0) return true;
   // blocks of <= 128 KB (n <= 128) stream fast enough through one SM even on narrow levels and
   // the serial base; n = 192, 256 only when the level has many segments
   return d <= 4 && (n <= 128 || (n <= 256 && K >= 64));
@@ -748,6 +753,15 @@ cudaError_t launch_wide_dc(const btd::SolveArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_wide(const btd::SolveArgs& a, cudaStream_t s) {
+  if (a.d >= 5) {
+    const size_t smem = (size_t)5 * a.n * btd::kDmmaDS * sizeof(double);
+    cudaError_t e = ensure_smem((const void*)btd::solve_dmma_kernel, smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)((a.d + btd::kDmmaDS - 1) / btd::kDmmaDS), (unsigned)(a.mode == btd::kSolveBase ? 1 : a.K));
+    btd::solve_dmma_kernel<<<grid, btd::kWideThreads, smem, s>>>(a);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+  }
   if (a.d == 1) return launch_wide_dc<1>(a, s);
   if (a.d == 2) return launch_wide_dc<2>(a, s);
   return launch_wide_dc<4>(a, s);

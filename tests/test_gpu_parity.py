@@ -77,6 +77,8 @@ SWEEP = [  # (N, n, d, crossover, rho)
     (90, 80, 2, 8, 4), (40, 100, 1, 64, 8), (25, 65, 3, 4, 2), (12, 150, 2, 2, 2),
     # n > 64, d <= 4, >= 64 segments per level: solve_wide_kernel (btd_solve3.cuh)
     (700, 128, 3, 64, 8), (600, 192, 1, 64, 8), (650, 100, 2, 64, 8),
+    # n > 64 with 5 <= d <= 8: solve_dmma_kernel (levels, base)
+    (700, 128, 8, 64, 8), (90, 256, 6, 8, 4), (300, 100, 5, 16, 8),
 ]
 
 
