@@ -2048,13 +2048,18 @@ int btd_chol_batch(double* blocks, const int64_t strides[3], int64_t count, int6
     return BTD_ERR_INVALID_ARGUMENT;
   }
   if (count == 0) return BTD_OK;
-  const size_t smem = n <= btd::kSeamSmemMaxN ? (size_t)n * n * sizeof(double) : 0;
-  cudaError_t e = ensure_smem((const void*)btd::seam_chol_kernel, smem);
-  if (e != cudaSuccess) return cuda_fail(st, e, "btd_chol_batch(attr)");
-  btd::seam_chol_kernel<<<(unsigned)count, btd::kSeamThreads, smem, (cudaStream_t)stream>>>(
-      blocks, to_strides(strides), (int)n, (long long)block_coord, (btd::SeamErr*)err);
+  if (n <= btd::kSeamSmemMaxN) {
+    const size_t smem = btd::seam_chol_smem((int)n);
+    cudaError_t e = ensure_smem((const void*)btd::seam_chol_smem_kernel, smem);
+    if (e != cudaSuccess) return cuda_fail(st, e, "btd_chol_batch(attr)");
+    btd::seam_chol_smem_kernel<<<(unsigned)count, btd::kSeamThreads, smem, (cudaStream_t)stream>>>(
+        blocks, to_strides(strides), (int)n, (long long)block_coord, (btd::SeamErr*)err);
+  } else {
+    btd::seam_chol_kernel<<<(unsigned)count, btd::kSeamThreads, 0, (cudaStream_t)stream>>>(
+        blocks, to_strides(strides), (int)n, (long long)block_coord, (btd::SeamErr*)err);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  e = cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BTD_OK : cuda_fail(st, e, "btd_chol_batch");
 }
 
@@ -2071,12 +2076,18 @@ int btd_trsm_batch(const double* factors, const int64_t fstrides[3], double* pan
   btd::seam_diag_check_kernel<<<(unsigned)count, 128, 0, s>>>(factors, to_strides(fstrides), (int)n, count,
                                                               (btd::SeamErr*)err);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (cols > 0) {
-    const size_t smem = n <= btd::kSeamSmemMaxN ? (size_t)n * n * sizeof(double) : 0;
-    cudaError_t e = ensure_smem((const void*)btd::seam_trsm_kernel, smem);
+  if (cols > 0 && n <= btd::kSeamSmemMaxN) {
+    const size_t smem = btd::seam_trsm_smem((int)n);
+    cudaError_t e = ensure_smem((const void*)btd::seam_trsm_dmma_kernel, smem);
     if (e != cudaSuccess) return cuda_fail(st, e, "btd_trsm_batch(attr)");
+    dim3 grid((unsigned)count, (unsigned)((cols + btd::kStCols - 1) / btd::kStCols));
+    btd::seam_trsm_dmma_kernel<<<grid, btd::kSeamThreads, smem, s>>>(factors, to_strides(fstrides), panels,
+                                                                      to_strides(pstrides), (int)n, (int)cols, trans,
+                                                                      (const btd::SeamErr*)err);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  } else if (cols > 0) {
     dim3 grid((unsigned)count, (unsigned)((cols + btd::kSeamThreads - 1) / btd::kSeamThreads));
-    btd::seam_trsm_kernel<<<grid, btd::kSeamThreads, smem, s>>>(factors, to_strides(fstrides), panels,
+    btd::seam_trsm_kernel<<<grid, btd::kSeamThreads, 0, s>>>(factors, to_strides(fstrides), panels,
                                                                  to_strides(pstrides), (int)n, (int)cols, trans,
                                                                  (const btd::SeamErr*)err);
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -2098,7 +2109,7 @@ int btd_gemm_batch(double* out, const int64_t ostrides[3], const double* a, cons
   btd::Strides as = to_strides(astrides), bs = to_strides(bstrides);
   if (trans_a) std::swap(as.r, as.c);  // op(a)(r, k) = a(k, r)
   if (trans_b) std::swap(bs.r, bs.c);
-  const int tiles_m = (int)((m + btd::kSeamTile - 1) / btd::kSeamTile), tiles_p = (int)((p + btd::kSeamTile - 1) / btd::kSeamTile);
+  const int tiles_m = (int)((m + btd::kSgT - 1) / btd::kSgT), tiles_p = (int)((p + btd::kSgT - 1) / btd::kSgT);
   dim3 grid((unsigned)(tiles_m * tiles_p), (unsigned)count);
   btd::seam_gemm_kernel<<<grid, btd::kSeamThreads, 0, (cudaStream_t)stream>>>(
       out, to_strides(ostrides), a, as, b, bs, (int)m, (int)q, (int)p, tiles_p, alpha, beta);

@@ -127,6 +127,9 @@ def _build_batched(model: StateSpaceModel, dev):
 
     def chol(x):  # (factor, (first failing member, pivot) or None)
         f = x.clone()
+        if f.shape[1] > _TRSM_BLOCK and chol_blocked(f):
+            return f, None
+        f = x.clone()  # unblocked (or after a failure: the exact first failing member and pivot)
         err = kn._ErrWord()
         kn._chol_dev(kn._Dev(f, True), f.shape[0], f.shape[1], err)
         rc, st = err.read()
@@ -166,6 +169,26 @@ def _build_batched(model: StateSpaceModel, dev):
                 gemm(panel[:, i0:i1], f[:, i1:, i0:i1], panel[:, i1:], ta=True, alpha=-1.0, beta=1.0)
             trsm1(f[:, i0:i1, i0:i1], panel[:, i0:i1], trans)
         return panel
+
+    def chol_blocked(f):
+        # right-looking blocked Cholesky over diagonal blocks of <= _TRSM_BLOCK (factored in shared
+        # memory by the seam kernel), L21 = A21 L11^{-T} as a seam trsm on the transposed view, the
+        # trailing update as a seam GEMM; True when every member is SPD (else the caller reruns the
+        # unblocked kernel for the reference's first failing member and pivot)
+        cnt, nn = f.shape[0], f.shape[1]
+        err = kn._ErrWord()
+        for i0 in range(0, nn, _TRSM_BLOCK):
+            i1 = min(nn, i0 + _TRSM_BLOCK)
+            d = f[:, i0:i1, i0:i1]
+            kn._chol_dev(kn._Dev(d, True), cnt, i1 - i0, err)
+            if i1 < nn:
+                pan = f[:, i1:, i0:i1]
+                kn._trsm_dev(kn._Dev(d, False), kn._Dev(pan.transpose(1, 2), True), cnt, i1 - i0, nn - i1, False, err)
+                gemm(f[:, i1:, i1:], pan, pan.transpose(1, 2), alpha=-1.0, beta=1.0)
+        if err.read()[0] != _native.BTD_OK:
+            return False
+        f.tril_()  # the original A12 and the square trailing updates above the diagonal
+        return True
 
     def spd_solve(f, panel):  # _chol_solve_spd (kalman.py:99-104)
         trsm(f, panel, False)

@@ -72,7 +72,8 @@ def test_trsm_known_answers(rng):
         trsm_lower(np.eye(3), np.ones((2, 1)))
 
 
-@pytest.mark.parametrize("n,d", [(3, 1), (16, 5), (64, 2), (96, 3), (130, 4), (200, 300)])
+@pytest.mark.parametrize("n,d", [(3, 1), (16, 5), (57, 64), (64, 2), (96, 3), (120, 65), (128, 150), (130, 4),
+                                 (200, 300)])
 def test_trsm_matches_solve(n, d, rng):
     f = np.linalg.cholesky(spd(n, rng))
     p = rng.standard_normal((n, d))
