@@ -158,6 +158,19 @@ def test_batch_failures_report_lowest_member(rng):
     assert np.array_equal(panels, np.ones((4, 2, 1)))  # nothing solved
 
 
+@pytest.mark.parametrize("n,k", [(40, 20), (128, 100), (100, 7), (200, 150)])
+def test_failure_pivot_past_the_first_panel(n, k, rng):
+    """The shared-memory kernel factors in 8-column panels: the failing pivot is still the first
+    non-positive one, 1-based, and the lowest failing member wins (member 1 fails later in the
+    elimination than member 2)."""
+    stack = np.stack([spd(n, rng) for _ in range(3)])
+    stack[1, k, k] = -1.0
+    stack[2, 2, 2] = -1.0
+    with pytest.raises(NotPositiveDefinite) as e:
+        chol_factor_batch(stack)
+    assert (e.value.member, e.value.pivot) == (1, k + 1)
+
+
 def test_thread_cap_is_an_api_knob_only(rng, monkeypatch):
     stack = np.stack([spd(4, rng) for _ in range(512)])
     stack[400] = -np.eye(4)
