@@ -377,11 +377,21 @@ void decode_error(const btd::DevErr& e, btd_status* st) {
 }
 
 int finish_check(btd_hierarchy* h, cudaStream_t stream, btd_status* st) {
-  btd::DevErr herr;
-  cudaError_t e = cudaMemcpyAsync(&herr, h->persistent + h->off_err, sizeof(herr), cudaMemcpyDeviceToHost, stream);
+  // the error word lands in a pinned per-thread word (a pageable destination goes through a driver
+  // staging copy, on the critical path between the last factor kernel and the caller's next launch);
+  // consumed before this thread's next factorization, so one word per thread serves every device
+  thread_local btd::DevErr* pinned = nullptr;
+  if (!pinned && cudaHostAlloc((void**)&pinned, sizeof(btd::DevErr), cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    pinned = nullptr;
+  }
+  btd::DevErr local;
+  btd::DevErr* dst = pinned ? pinned : &local;
+  cudaError_t e = cudaMemcpyAsync(dst, h->persistent + h->off_err, sizeof(btd::DevErr), cudaMemcpyDeviceToHost, stream);
   if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(copy error word)");
   e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) return cuda_fail(st, e, "btd_factorize(sync)");
+  const btd::DevErr herr = *dst;
   h->pending_check = false;
   if (herr.key != btd::kNoErr) {
     h->factored = false;

@@ -206,6 +206,11 @@ def _on_stream(device, stream):
     non-current stream is safe in both directions; the caching allocator attributes every
     temporary to ``stream``."""
     import torch
+    if stream is None and device.index == torch.cuda.current_device():
+        # the common call: nothing to switch (entering torch's stream context costs ~10 us of host
+        # time, on the critical path between a factorization's error check and the solve launch)
+        yield torch.cuda.current_stream(device)
+        return
     with torch.cuda.device(device):
         cur = torch.cuda.current_stream(device)
         s = stream if stream is not None else cur
@@ -320,7 +325,8 @@ def _solve_on(hierarchy, rhs, s):
         b = rhs.blocks
         if b.device != native.device:
             b = b.to(native.device, non_blocking=True)
-        b = b.to(torch.float64).contiguous()
+        if b.dtype != torch.float64 or not b.is_contiguous():
+            b = b.to(torch.float64).contiguous()
     d = int(b.shape[2])
     npad = getattr(native, "padded", hierarchy.block_size)
     nu = hierarchy.block_size
