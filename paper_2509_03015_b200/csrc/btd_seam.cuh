@@ -32,23 +32,30 @@ __global__ void seam_err_init_kernel(SeamErr* e) {
   e->sing = kNoErr;
 }
 
-// Shared-memory staging of total elements (index e -> value via src, stored via dst), 8 loads in
-// flight per thread so a lone CTA is not bound by one L2 round trip per element.
+// Visit every (r, c) of an R x C window with lanes along the unit-stride axis (cfast: columns) and
+// warps plus an 8-deep unroll along the other, so a lone CTA keeps 8 loads per thread in flight
+// instead of one L2 round trip per element; no integer division in the index math.
 template <class Src, class Dst>
-__device__ __forceinline__ void seam_stage(int total, Src src, Dst dst) {
-  for (int base = 0; base < total; base += kSeamThreads * 8) {
-    double v[8];
+__device__ __forceinline__ void seam_stage(int R, int C, bool cfast, Src src, Dst dst) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kSeamThreads / 32;
+  const int outer = cfast ? R : C, inner = cfast ? C : R;
+  for (int b = lane; b < inner; b += 32)
+    for (int a0 = warp; a0 < outer; a0 += nw * 8) {
+      double v[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int e = base + q * kSeamThreads + threadIdx.x;
-      v[q] = e < total ? src(e) : 0.0;
-    }
+      for (int q = 0; q < 8; ++q) {
+        const int a = a0 + q * nw;
+        v[q] = a < outer ? (cfast ? src(a, b) : src(b, a)) : 0.0;
+      }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int e = base + q * kSeamThreads + threadIdx.x;
-      if (e < total) dst(e, v[q]);
+      for (int q = 0; q < 8; ++q) {
+        const int a = a0 + q * nw;
+        if (a < outer) {
+          if (cfast) dst(a, b, v[q]);
+          else dst(b, a, v[q]);
+        }
+      }
     }
-  }
 }
 
 __host__ __device__ constexpr int seam_np(int n) { return (n + 7) & ~7; }  // padded to whole 8-row blocks
@@ -80,15 +87,11 @@ __global__ void __launch_bounds__(kSeamThreads) seam_chol_smem_kernel(double* a,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool cfast = llabs(s.c) <= llabs(s.r);
   seam_stage(
-      NP * NP,
-      [&](int e) {
-        const int r = cfast ? e / NP : e % NP, c = cfast ? e % NP : e / NP;
+      NP, NP, cfast,
+      [&](int r, int c) {
         return (r < n && c <= r) ? A[(long long)r * s.r + (long long)c * s.c] : (r == c ? 1.0 : 0.0);
       },
-      [&](int e, double v) {
-        const int r = cfast ? e / NP : e % NP, c = cfast ? e % NP : e / NP;
-        sw[r * LL + c] = v;
-      });
+      [&](int r, int c, double v) { sw[r * LL + c] = v; });
   __syncthreads();
   int fail = 0;
   for (int j0 = 0; j0 < NP; j0 += 8) {
@@ -157,10 +160,9 @@ __global__ void __launch_bounds__(kSeamThreads) seam_chol_smem_kernel(double* a,
     }
     return;
   }
-  for (int e = tid; e < n * n; e += kSeamThreads) {
-    const int r = cfast ? e / n : e % n, c = cfast ? e % n : e / n;
-    A[(long long)r * s.r + (long long)c * s.c] = c > r ? 0.0 : sw[r * LL + c];
-  }
+  seam_stage(
+      n, n, cfast, [&](int r, int c) { return c > r ? 0.0 : sw[r * LL + c]; },
+      [&](int r, int c, double v) { A[(long long)r * s.r + (long long)c * s.c] = v; });
 }
 
 // The same for members larger than kSeamSmemMaxN: one CTA per member, right-looking column
@@ -283,25 +285,17 @@ __global__ void __launch_bounds__(kSeamThreads) seam_trsm_dmma_kernel(const doub
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool f_cfast = llabs(fs.c) <= llabs(fs.r), p_cfast = llabs(ps.c) <= llabs(ps.r);
   seam_stage(
-      NP * NP,
-      [&](int e) {
-        const int r = f_cfast ? e / NP : e % NP, c = f_cfast ? e % NP : e / NP;
+      NP, NP, f_cfast,
+      [&](int r, int c) {
         return (r < n && c <= r) ? F[(long long)r * fs.r + (long long)c * fs.c] : (r == c ? 1.0 : 0.0);
       },
-      [&](int e, double v) {
-        const int r = f_cfast ? e / NP : e % NP, c = f_cfast ? e % NP : e / NP;
-        Ls[r * LL + c] = v;
-      });
+      [&](int r, int c, double v) { Ls[r * LL + c] = v; });
   seam_stage(
-      NP * kStCols,
-      [&](int e) {
-        const int r = p_cfast ? e / kStCols : e % NP, c = p_cfast ? e % kStCols : e / NP;
+      NP, kStCols, p_cfast,
+      [&](int r, int c) {
         return (r < n && c < w) ? P[(long long)r * ps.r + (long long)(col0 + c) * ps.c] : 0.0;
       },
-      [&](int e, double v) {
-        const int r = p_cfast ? e / kStCols : e % NP, c = p_cfast ? e % kStCols : e / NP;
-        Xs[r * kStLX + c] = v;
-      });
+      [&](int r, int c, double v) { Xs[r * kStLX + c] = v; });
   __syncthreads();
   const int nb = NP / 8;
   for (int s = 0; s < nb; ++s) {
@@ -355,10 +349,9 @@ __global__ void __launch_bounds__(kSeamThreads) seam_trsm_dmma_kernel(const doub
     }
     __syncthreads();
   }
-  for (int e = tid; e < NP * kStCols; e += kSeamThreads) {
-    const int r = p_cfast ? e / kStCols : e % NP, c = p_cfast ? e % kStCols : e / NP;
-    if (r < n && c < w) P[(long long)r * ps.r + (long long)(col0 + c) * ps.c] = Xs[r * kStLX + c];
-  }
+  seam_stage(
+      n, w, p_cfast, [&](int r, int c) { return Xs[r * kStLX + c]; },
+      [&](int r, int c, double v) { P[(long long)r * ps.r + (long long)(col0 + c) * ps.c] = v; });
 }
 
 // out <- alpha op(a) op(b) + beta out per member (gemm_acc_batch, kernels.py:270-310).  The operand
