@@ -744,12 +744,20 @@ __global__ void __launch_bounds__(FactorShape<NT>::NTHREADS, FactorShape<NT>::MI
         dacc[i][0] = dacc[i][1] = 0.0;
       }
       const double* base = XP + (lane >> 2) * LD + (lane & 3);
+      // a warp's tiles lie in at most two tile rows (7 - pr and pr): one A fragment load per row
+      // and k step, shared by the tiles of that row (7 instead of 10 fragment loads per k step)
+      bool rhi[5];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) rhi[i] = dtr[i] == 7 - pr;
+      const double* pah = base + (7 - pr) * 8 * LD;
+      const double* pal = base + pr * 8 * LD;
 #pragma unroll 4
       for (int k0 = 0; k0 < NT; k0 += 4) {
+        const double ah = pah[k0], al = pal[k0];
 #pragma unroll
         for (int i = 0; i < 5; ++i) {
           if (dtr[i] < 0) continue;
-          dmma(dacc[i], base[dtr[i] * 8 * LD + k0], base[dtc[i] * 8 * LD + k0]);
+          dmma(dacc[i], rhi[i] ? ah : al, base[dtc[i] * 8 * LD + k0]);
         }
       }
       cp_async_wait_all();
