@@ -417,8 +417,19 @@ __global__ void __launch_bounds__(BTHREADS) big_potrf_kernel(BigPotrfArgs g) {
       __syncthreads();
       for (int e = tid; e < BT * BT; e += BTHREADS) DL[(e / BT) * LD + e % BT] = D[(size_t)(kb * BT + e / BT) * n + kb * BT + e % BT];
       __syncthreads();
+      // the single-warp left-looking pivot chain, then the inverse by recursive doubling on
+      // group A (the schedule of factor_level_kernel<64>)
       int fail = 0;
-      if (warp < S::NWA) fail = potrf_trtri<64>(DL, &s_fail);
+      if (warp < S::NWA) {
+        if (warp == 0) {
+          const int f = chain_potrf<LD, 64>(DL, lane);
+          if (lane == 0) s_fail = f;
+        }
+        named_sync(kBarA, S::NWA * 32);
+        fail = s_fail;
+        if (!fail) trtri_doubling<64>(DL, warp, lane);
+      }
+      __syncthreads();
       if (tid == 0) s_fail = fail;
       __syncthreads();
       if (s_fail) {
