@@ -320,7 +320,7 @@ def run_ours(args, rank, world):
 
     # per-launch timing of the dominant kernel (level-0 factor) through the C-ABI timing hook
     h = X = None
-    kt = pkg.schur.factor_kernel_times(dA, repeats=3)
+    kt = pkg.schur.factor_kernel_times(dA, repeats=3, rhs_cols=d)
     clocks = sampler.stop(dev.index) if sampler else None
     del dA, dB
     torch.cuda.empty_cache()  # the host-input path below allocates its own device arenas

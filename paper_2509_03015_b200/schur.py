@@ -356,14 +356,15 @@ def _solve_on(hierarchy, rhs, s):
 
 
 def factor_kernel_times(matrix: BlockTridiagonalMatrix, config: RecursionConfig | None = None,
-                        repeats: int = 3) -> dict:
-    """Bench helper: median (over ``repeats``) device times of factor, solve and the level-0 factor
-    kernel (CUDA events on the launching stream, C-ABI timing hook)."""
+                        repeats: int = 3, rhs_cols: int = 1) -> dict:
+    """Bench helper: median (over ``repeats``) device times of factor, solve (``rhs_cols``
+    right-hand sides) and the level-0 factor kernel (CUDA events on the launching stream, C-ABI
+    timing hook)."""
     import statistics
 
     import torch
     f_ms, s_ms, l0 = [], [], []
-    rhs = BlockRhs(torch.ones((matrix.num_blocks, matrix.block_size, 1), dtype=torch.float64,
+    rhs = BlockRhs(torch.ones((matrix.num_blocks, matrix.block_size, rhs_cols), dtype=torch.float64,
                               device=matrix.diag.device))
     h = None
     for _ in range(repeats):
