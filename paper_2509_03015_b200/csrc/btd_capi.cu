@@ -315,11 +315,11 @@ cudaError_t launch_stream_v(const btd::SolveArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// Wide levels (at least as many segments as SMs) at n = 64, d = 1 run two CTAs per SM; narrow
-// levels and the base keep one CTA per SM with a 4-slot ring (deeper prefetch for the lone segment).
+// Wide levels (at least as many segments as SMs) at n = 64 run two CTAs per SM; narrow levels and
+// the base keep one CTA per SM with a deeper ring (more prefetch for the lone segment).
 template <int NT, int DC>
 cudaError_t launch_stream(const btd::SolveArgs& a, cudaStream_t s) {
-  if constexpr (NT == 64 && DC == 1) {
+  if constexpr (NT == 64) {
     if (a.mode != btd::kSolveBase && a.K >= device_sms()) return launch_stream_v<NT, DC, true>(a, s);
   }
   return launch_stream_v<NT, DC, false>(a, s);

@@ -190,6 +190,56 @@ __device__ __forceinline__ void mtv(const double* __restrict__ M, const double* 
     }
 }
 
+// Transposed form at NT == 64, DC == 4 on all 8 consumer warps (the 4-warp mtv leaves half the
+// consumers idle on the backward sweep, the longer half of the step at d = 4): warp w owns the 8
+// columns 8w..8w+7, lane = column pair p (lane % 4) + 4 part, part sweeping rows part, part + 8, ...
+// The 8 partials of a lane (2 columns x 4 rhs columns) are reduced over the 8 parts by a
+// transposing butterfly (4 + 2 + 1 shuffles): lane (p, part) ends with the total of column
+// 8w + 2p + (part >> 2), rhs column part & 3.
+template <bool PACKED>
+__device__ __forceinline__ double mtv64x4(const double* __restrict__ M, const double* __restrict__ x, int& col,
+                                          int& rc) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int part = lane >> 2, c2 = 8 * w + 2 * (lane & 3);
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int m = part + 8 * i;
+    double2 e = make_double2(0.0, 0.0);
+    if (!PACKED) e = *reinterpret_cast<const double2*>(M + m * 64 + c2);
+    else if (c2 <= m) e = *reinterpret_cast<const double2*>(M + packed_row_offset(m) + c2);
+    const double2 x01 = *reinterpret_cast<const double2*>(x + m * 4);
+    const double2 x23 = *reinterpret_cast<const double2*>(x + m * 4 + 2);
+    a[0] = fma(e.x, x01.x, a[0]);
+    a[1] = fma(e.x, x01.y, a[1]);
+    a[2] = fma(e.x, x23.x, a[2]);
+    a[3] = fma(e.x, x23.y, a[3]);
+    a[4] = fma(e.y, x01.x, a[4]);
+    a[5] = fma(e.y, x01.y, a[5]);
+    a[6] = fma(e.y, x23.x, a[6]);
+    a[7] = fma(e.y, x23.y, a[7]);
+  }
+  const bool b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double snd = b4 ? a[i] : a[i + 4], kp = b4 ? a[i + 4] : a[i];
+    a[i] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double snd = b3 ? a[i] : a[i + 2], kp = b3 ? a[i + 2] : a[i];
+    a[i] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+  }
+  const double snd = b2 ? a[0] : a[1], kp = b2 ? a[1] : a[0];
+  const double v = kp + __shfl_xor_sync(0xffffffffu, snd, 4);
+  // value index 4 b4 + 2 b3 + b2 = part: column half b4, rhs column 2 b3 + b2
+  col = c2 + (part >> 2);
+  rc = part & 3;
+  return v;
+}
+
 // Row form at NT == 64 without the rotated reads: warp w owns rows 8w..8w+7 and lane l the column
 // pair (2l, 2l+1), so each row read is one contiguous conflict-free 512-byte run and x[2l..2l+1]
 // is loaded once into registers; the 8 row partials are reduced across the warp by a
@@ -283,18 +333,21 @@ struct SegBounds {
   }
 };
 
-// WIDE (levels with at least as many segments as SMs, n = 64, d = 1): two CTAs per SM (two
-// segments in flight per SM) with 2-slot rings; otherwise one CTA per SM with a deeper ring.
+// WIDE (levels with at least as many segments as SMs, n = 64, d <= 4): two CTAs per SM (two
+// segments in flight per SM) with 2-slot rings; otherwise one CTA per SM with a deeper ring.  With
+// d > 1 two CTAs' rings leave no room for the forward sweep's z cache (ZMAX = 0): z_j goes through
+// the solution buffer (L2) instead.
 template <int NT, int DC, bool WIDE = false>
 struct TmaShape {
   using S = Solve2Shape<NT>;
   static constexpr int NCW = S::NTHREADS / 32;  // consumer warps
   static constexpr int NTHREADS = S::NTHREADS + 32;
-  static constexpr bool TWO = WIDE && NT == 64 && DC == 1;
-  static constexpr int STAGES = NT == 64 ? (DC > 1 ? 3 : (TWO ? 2 : 4)) : 8;
+  static constexpr bool TWO = WIDE && NT == 64 && DC <= 4;
+  static constexpr int STAGES = NT == 64 ? (TWO ? 2 : (DC > 1 ? 3 : 4)) : 8;
   static constexpr int STAGE = S::FULL + S::PACK + NT * DC;  // doubles per slot
+  static constexpr int ZMAX = (TWO && DC > 1) ? 0 : S::ZMAX;
   static constexpr int MINB = TWO ? 2 : 1;  // resident CTAs per SM (register cap 112 when 2)
-  static constexpr size_t SMEM = sizeof(double) * ((size_t)STAGES * STAGE + (size_t)(4 + S::ZMAX) * NT * DC) +
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)STAGES * STAGE + (size_t)(4 + ZMAX) * NT * DC) +
                                  2 * STAGES * sizeof(unsigned long long);
 };
 
@@ -310,7 +363,7 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
   double* u = t + NT * DC;
   double* corr = u + NT * DC;
   double* zc = corr + 2 * NT * DC;
-  unsigned long long* full_bar = reinterpret_cast<unsigned long long*>(zc + S::ZMAX * NT * DC);
+  unsigned long long* full_bar = reinterpret_cast<unsigned long long*>(zc + T::ZMAX * NT * DC);
   unsigned long long* empty_bar = full_bar + STAGES;
   if (error_raised(a.err)) return;
   const int n = NT, d = a.d, mode = a.mode;
@@ -390,6 +443,7 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
   // transposed products (backward sweep, C_L fold) on the first TW warps with every part of a
   // column inside one warp (xor-shuffle reduction, no shared-memory partials).
   constexpr int TW = NT < 16 ? 1 : NT / 16;
+  constexpr bool X4 = NT == 64 && DC == 4;  // transposed products on all consumer warps
   constexpr int CW = NT < 16 ? NT : 16, PR = CW / 2;
   const int rr = tid >> 2;
   const bool rlead = (tid & 3) == 0;
@@ -446,7 +500,7 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
         double sm[DC];
         mv_packed_rows<NT, DC>(sp, t, sm);
         if (rlead) {
-          double* zdst = j < S::ZMAX ? zc + j * NT * DC : nullptr;
+          double* zdst = j < T::ZMAX ? zc + j * NT * DC : nullptr;
 #pragma unroll
           for (int c = 0; c < DC; ++c) {
             u[rr * DC + c] = sm[c];
@@ -458,13 +512,17 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
         csync<NT>();
         BTD_SPH(5);
       } else if (kind == kStepB) {
-        const double* zsrc = j < S::ZMAX ? zc + j * NT * DC : nullptr;
+        const double* zsrc = j < T::ZMAX ? zc + j * NT * DC : nullptr;
         auto zval = [&](int r, int c) -> double {
           return zsrc ? zsrc[r * DC + c] : (c < dc ? a.x[row * ps + (size_t)r * d + c0 + c] : 0.0);
         };
         const double* src = zsrc;
         if (j < J - 1) {  // t = z_j - L_{j+1,j}^T w_{j+1}
-          if (warp < TW) {
+          if constexpr (X4) {
+            int oc, orc;
+            const double ov = mtv64x4<false>(sf, u, oc, orc);
+            t[oc * DC + orc] = zval(oc, orc) - ov;
+          } else if (warp < TW) {
             double v[2][DC];
             mtv<NT, DC, false>(sf, u, v);
             if (tlead) {
@@ -485,7 +543,12 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
           src = t;
         }
         // w_j = Linv_j^T t
-        if (warp < TW) {
+        if constexpr (X4) {
+          int oc, orc;
+          const double ov = mtv64x4<true>(sp, src, oc, orc);
+          u[oc * DC + orc] = ov;
+          if (mode != kSolveDown && orc < dc) a.x[row * ps + (size_t)oc * d + c0 + orc] = ov;
+        } else if (warp < TW) {
           double v[2][DC];
           mtv<NT, DC, true>(sp, src, v);
           if (tlead) {
@@ -511,6 +574,10 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
             for (int c = 0; c < DC; ++c)
               if (c < dc) dst[(size_t)rr * d + c0 + c] = sm[c];
           }
+        } else if constexpr (X4) {
+          int oc, orc;
+          const double ov = mtv64x4<false>(sf, u, oc, orc);
+          if (orc < dc) dst[(size_t)oc * d + c0 + orc] = ov;
         } else if (warp < TW) {
           double v[2][DC];
           mtv<NT, DC, false>(sf, u, v);
@@ -542,6 +609,10 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
 #pragma unroll
             for (int c = 0; c < DC; ++c) corr[rr * DC + c] = sm[c];
           }
+        } else if constexpr (X4) {
+          int oc, orc;
+          const double ov = mtv64x4<false>(sf, t, oc, orc);
+          corr[NT * DC + oc * DC + orc] = ov;
         } else if (warp < TW) {
           double v[2][DC];
           mtv<NT, DC, false>(sf, t, v);

@@ -79,6 +79,10 @@ SWEEP = [  # (N, n, d, crossover, rho)
     (700, 128, 3, 64, 8), (600, 192, 1, 64, 8), (650, 100, 2, 64, 8),
     # n > 64 with 5 <= d <= 8: solve_dmma_kernel (levels, base)
     (700, 128, 8, 64, 8), (90, 256, 6, 8, 4), (300, 100, 5, 16, 8),
+    # n <= 64 with d > 1 and >= #SMs segments: two-CTA solve_tma_kernel (z through the solution
+    # buffer), incl. column slices (d > 4), padded blocks and long segments
+    (1500, 64, 4, 64, 8), (1400, 64, 2, 64, 8), (1500, 64, 7, 64, 8), (1600, 50, 3, 64, 8),
+    (2600, 64, 4, 64, 16),
 ]
 
 
