@@ -195,7 +195,7 @@ __device__ __forceinline__ void mtv(const double* __restrict__ M, const double* 
 // columns 8w..8w+7, lane = column pair p (lane % 4) + 4 part, part sweeping rows part, part + 8, ...
 // The 8 partials of a lane (2 columns x 4 rhs columns) are reduced over the 8 parts by a
 // transposing butterfly (4 + 2 + 1 shuffles): lane (p, part) ends with the total of column
-// 8w + 2p + (part >> 2), rhs column part & 3.
+// 8w + 2p + (part >> 2), rhs column part & 3.  x is column-major (x[c][64]).
 template <bool PACKED>
 __device__ __forceinline__ double mtv64x4(const double* __restrict__ M, const double* __restrict__ x, int& col,
                                           int& rc) {
@@ -210,16 +210,15 @@ __device__ __forceinline__ double mtv64x4(const double* __restrict__ M, const do
     double2 e = make_double2(0.0, 0.0);
     if (!PACKED) e = *reinterpret_cast<const double2*>(M + m * 64 + c2);
     else if (c2 <= m) e = *reinterpret_cast<const double2*>(M + packed_row_offset(m) + c2);
-    const double2 x01 = *reinterpret_cast<const double2*>(x + m * 4);
-    const double2 x23 = *reinterpret_cast<const double2*>(x + m * 4 + 2);
-    a[0] = fma(e.x, x01.x, a[0]);
-    a[1] = fma(e.x, x01.y, a[1]);
-    a[2] = fma(e.x, x23.x, a[2]);
-    a[3] = fma(e.x, x23.y, a[3]);
-    a[4] = fma(e.y, x01.x, a[4]);
-    a[5] = fma(e.y, x01.y, a[5]);
-    a[6] = fma(e.y, x23.x, a[6]);
-    a[7] = fma(e.y, x23.y, a[7]);
+    const double x0 = x[m], x1 = x[64 + m], x2 = x[128 + m], x3 = x[192 + m];  // x[c][64]
+    a[0] = fma(e.x, x0, a[0]);
+    a[1] = fma(e.x, x1, a[1]);
+    a[2] = fma(e.x, x2, a[2]);
+    a[3] = fma(e.x, x3, a[3]);
+    a[4] = fma(e.y, x0, a[4]);
+    a[5] = fma(e.y, x1, a[5]);
+    a[6] = fma(e.y, x2, a[6]);
+    a[7] = fma(e.y, x3, a[7]);
   }
   const bool b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1;
 #pragma unroll
@@ -245,12 +244,22 @@ __device__ __forceinline__ double mtv64x4(const double* __restrict__ M, const do
 // is loaded once into registers; the 8 row partials are reduced across the warp by a
 // transposing butterfly (4 + 2 + 1 + 2 shuffles).  The total of row 8w + lane/4 (= tid/4, the
 // mv_rows mapping) is returned on the 4 lanes of that row's quad.
-template <int DC, bool PACKED>
+// XT: x is stored column-major (x[c][64], see solve_tma_kernel's vidx), so lane l's pair of
+// entries of each rhs column is one conflict-free 16-byte read (row-major at d = 4 put the 32 lanes'
+// reads 64 bytes apart: 16 shared-memory wavefronts per load instead of 4).
+template <int DC, bool PACKED, bool XT = false>
 __device__ __forceinline__ void mv64(const double* __restrict__ M, const double* __restrict__ x, double (&s)[DC]) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c2 = 2 * lane;
   double x0[DC], x1[DC], v[8][DC];
-  if (DC == 1) {
+  if constexpr (XT) {
+#pragma unroll
+    for (int c = 0; c < DC; ++c) {
+      const double2 xv = *reinterpret_cast<const double2*>(x + c * 64 + c2);
+      x0[c] = xv.x;
+      x1[c] = xv.y;
+    }
+  } else if (DC == 1) {
     const double2 xv = *reinterpret_cast<const double2*>(x + c2);
     x0[0] = xv.x;
     x1[0] = xv.y;
@@ -296,12 +305,12 @@ __device__ __forceinline__ void mv64(const double* __restrict__ M, const double*
 
 template <int NT, int DC>
 __device__ __forceinline__ void mv_full_rows(const double* M, const double* x, double (&s)[DC]) {
-  if constexpr (NT == 64) { mv64<DC, false>(M, x, s); return; }
+  if constexpr (NT == 64) { mv64<DC, false, DC == 4>(M, x, s); return; }
   mv_rows<NT, DC>(M, x, s);
 }
 template <int NT, int DC>
 __device__ __forceinline__ void mv_packed_rows(const double* M, const double* x, double (&s)[DC]) {
-  if constexpr (NT == 64) { mv64<DC, true>(M, x, s); return; }
+  if constexpr (NT == 64) { mv64<DC, true, DC == 4>(M, x, s); return; }
   mv_pack_rows<NT, DC>(M, x, s);
 }
 
@@ -444,6 +453,8 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
   // column inside one warp (xor-shuffle reduction, no shared-memory partials).
   constexpr int TW = NT < 16 ? 1 : NT / 16;
   constexpr bool X4 = NT == 64 && DC == 4;  // transposed products on all consumer warps
+  // shared-memory vectors (t, u, z cache, corrections): row-major [r][c], column-major at X4
+  auto vi = [](int r, int c) { return X4 ? c * NT + r : r * DC + c; };
   constexpr int CW = NT < 16 ? NT : 16, PR = CW / 2;
   const int rr = tid >> 2;
   const bool rlead = (tid & 3) == 0;
@@ -475,8 +486,8 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
         double v = 0.0;
         if (c < dc) v = vec_bulk ? sv[r * d + c] : a.rhs[row * ps + (size_t)r * d + c0 + c];
         if (mode == kSolveUp) {
-          if (j == 0) v -= corr[r * DC + c];
-          if (j == J - 1) v -= corr[NT * DC + r * DC + c];
+          if (j == 0) v -= corr[vi(r, c)];
+          if (j == J - 1) v -= corr[NT * DC + vi(r, c)];
         }
         return v;
       };
@@ -488,10 +499,10 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
           mv_full_rows<NT, DC>(sf, u, sm);
           if (rlead) {
 #pragma unroll
-            for (int c = 0; c < DC; ++c) t[rr * DC + c] = bval(rr, c) - sm[c];
+            for (int c = 0; c < DC; ++c) t[vi(rr, c)] = bval(rr, c) - sm[c];
           }
         } else {
-          for (int e = tid; e < NT * DC; e += NTH) t[e] = bval(e / DC, e % DC);
+          for (int e = tid; e < NT * DC; e += NTH) t[vi(e / DC, e % DC)] = bval(e / DC, e % DC);
         }
         BTD_SPH(2);
         csync<NT>();
@@ -503,8 +514,8 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
           double* zdst = j < T::ZMAX ? zc + j * NT * DC : nullptr;
 #pragma unroll
           for (int c = 0; c < DC; ++c) {
-            u[rr * DC + c] = sm[c];
-            if (zdst) zdst[rr * DC + c] = sm[c];
+            u[vi(rr, c)] = sm[c];
+            if (zdst) zdst[vi(rr, c)] = sm[c];
             else if (c < dc) a.x[row * ps + (size_t)rr * d + c0 + c] = sm[c];
           }
         }
@@ -514,22 +525,22 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
       } else if (kind == kStepB) {
         const double* zsrc = j < T::ZMAX ? zc + j * NT * DC : nullptr;
         auto zval = [&](int r, int c) -> double {
-          return zsrc ? zsrc[r * DC + c] : (c < dc ? a.x[row * ps + (size_t)r * d + c0 + c] : 0.0);
+          return zsrc ? zsrc[vi(r, c)] : (c < dc ? a.x[row * ps + (size_t)r * d + c0 + c] : 0.0);
         };
         const double* src = zsrc;
         if (j < J - 1) {  // t = z_j - L_{j+1,j}^T w_{j+1}
           if constexpr (X4) {
             int oc, orc;
             const double ov = mtv64x4<false>(sf, u, oc, orc);
-            t[oc * DC + orc] = zval(oc, orc) - ov;
+            t[vi(oc, orc)] = zval(oc, orc) - ov;
           } else if (warp < TW) {
             double v[2][DC];
             mtv<NT, DC, false>(sf, u, v);
             if (tlead) {
 #pragma unroll
               for (int c = 0; c < DC; ++c) {
-                t[tc * DC + c] = zval(tc, c) - v[0][c];
-                t[(tc + 1) * DC + c] = zval(tc + 1, c) - v[1][c];
+                t[vi(tc, c)] = zval(tc, c) - v[0][c];
+                t[vi(tc + 1, c)] = zval(tc + 1, c) - v[1][c];
               }
             }
           }
@@ -538,7 +549,7 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
           BTD_SPH(7);
           src = t;
         } else if (!zsrc) {
-          for (int e = tid; e < NT * DC; e += NTH) t[e] = zval(e / DC, e % DC);
+          for (int e = tid; e < NT * DC; e += NTH) t[vi(e / DC, e % DC)] = zval(e / DC, e % DC);
           csync<NT>();
           src = t;
         }
@@ -546,7 +557,7 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
         if constexpr (X4) {
           int oc, orc;
           const double ov = mtv64x4<true>(sp, src, oc, orc);
-          u[oc * DC + orc] = ov;
+          u[vi(oc, orc)] = ov;
           if (mode != kSolveDown && orc < dc) a.x[row * ps + (size_t)oc * d + c0 + orc] = ov;
         } else if (warp < TW) {
           double v[2][DC];
@@ -556,7 +567,7 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
             for (int c = 0; c < DC; ++c)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
-                u[(tc + h) * DC + c] = v[h][c];
+                u[vi(tc + h, c)] = v[h][c];
                 if (mode != kSolveDown && c < dc) a.x[row * ps + (size_t)(tc + h) * d + c0 + c] = v[h][c];
               }
           }
@@ -594,7 +605,7 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
         for (int e = tid; e < NT * DC; e += NTH) {
           const int r = e / DC, c = e % DC;
           const double v = c < dc ? (vec_bulk ? sv[r * d + c] : xs[(size_t)r * d + c0 + c]) : 0.0;
-          t[e] = v;
+          t[vi(r, c)] = v;
           if (c < dc) {
             const size_t off = (size_t)r * d + c0 + c;
             if (kind == kStepCL) a.x[(size_t)(start - 1) * ps + off] = v;
@@ -607,20 +618,20 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
           mv_full_rows<NT, DC>(sf, t, sm);
           if (rlead) {
 #pragma unroll
-            for (int c = 0; c < DC; ++c) corr[rr * DC + c] = sm[c];
+            for (int c = 0; c < DC; ++c) corr[vi(rr, c)] = sm[c];
           }
         } else if constexpr (X4) {
           int oc, orc;
           const double ov = mtv64x4<false>(sf, t, oc, orc);
-          corr[NT * DC + oc * DC + orc] = ov;
+          corr[NT * DC + vi(oc, orc)] = ov;
         } else if (warp < TW) {
           double v[2][DC];
           mtv<NT, DC, false>(sf, t, v);
           if (tlead) {
 #pragma unroll
             for (int c = 0; c < DC; ++c) {
-              corr[NT * DC + tc * DC + c] = v[0][c];
-              corr[NT * DC + (tc + 1) * DC + c] = v[1][c];
+              corr[NT * DC + vi(tc, c)] = v[0][c];
+              corr[NT * DC + vi(tc + 1, c)] = v[1][c];
             }
           }
         }
