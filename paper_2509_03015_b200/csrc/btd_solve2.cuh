@@ -190,12 +190,16 @@ __device__ __forceinline__ void mtv(const double* __restrict__ M, const double* 
     }
 }
 
+// Column stride of the d = 4 shared-memory vectors (x[c][kXLD]): 72, not 64, so the transposed
+// product's one-value-per-lane stores (8 columns x 4 rhs columns per warp) fall in 2 wavefronts.
+constexpr int kXLD = 72;
+
 // Transposed form at NT == 64, DC == 4 on all 8 consumer warps (the 4-warp mtv leaves half the
 // consumers idle on the backward sweep, the longer half of the step at d = 4): warp w owns the 8
 // columns 8w..8w+7, lane = column pair p (lane % 4) + 4 part, part sweeping rows part, part + 8, ...
 // The 8 partials of a lane (2 columns x 4 rhs columns) are reduced over the 8 parts by a
 // transposing butterfly (4 + 2 + 1 shuffles): lane (p, part) ends with the total of column
-// 8w + 2p + (part >> 2), rhs column part & 3.  x is column-major (x[c][64]).
+// 8w + 2p + (part >> 2), rhs column part & 3.  x is column-major (x[c][kXLD]).
 template <bool PACKED>
 __device__ __forceinline__ double mtv64x4(const double* __restrict__ M, const double* __restrict__ x, int& col,
                                           int& rc) {
@@ -210,7 +214,7 @@ __device__ __forceinline__ double mtv64x4(const double* __restrict__ M, const do
     double2 e = make_double2(0.0, 0.0);
     if (!PACKED) e = *reinterpret_cast<const double2*>(M + m * 64 + c2);
     else if (c2 <= m) e = *reinterpret_cast<const double2*>(M + packed_row_offset(m) + c2);
-    const double x0 = x[m], x1 = x[64 + m], x2 = x[128 + m], x3 = x[192 + m];  // x[c][64]
+    const double x0 = x[m], x1 = x[kXLD + m], x2 = x[2 * kXLD + m], x3 = x[3 * kXLD + m];  // x[c][kXLD]
     a[0] = fma(e.x, x0, a[0]);
     a[1] = fma(e.x, x1, a[1]);
     a[2] = fma(e.x, x2, a[2]);
@@ -255,7 +259,7 @@ __device__ __forceinline__ void mv64(const double* __restrict__ M, const double*
   if constexpr (XT) {
 #pragma unroll
     for (int c = 0; c < DC; ++c) {
-      const double2 xv = *reinterpret_cast<const double2*>(x + c * 64 + c2);
+      const double2 xv = *reinterpret_cast<const double2*>(x + c * kXLD + c2);
       x0[c] = xv.x;
       x1[c] = xv.y;
     }
@@ -355,8 +359,9 @@ struct TmaShape {
   static constexpr int STAGES = NT == 64 ? (TWO ? 2 : (DC > 1 ? 3 : 4)) : 8;
   static constexpr int STAGE = S::FULL + S::PACK + NT * DC;  // doubles per slot
   static constexpr int ZMAX = (TWO && DC > 1) ? 0 : S::ZMAX;
+  static constexpr int VS = (NT == 64 && DC == 4) ? DC * kXLD : NT * DC;  // doubles per shared vector
   static constexpr int MINB = TWO ? 2 : 1;  // resident CTAs per SM (register cap 112 when 2)
-  static constexpr size_t SMEM = sizeof(double) * ((size_t)STAGES * STAGE + (size_t)(4 + ZMAX) * NT * DC) +
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)STAGES * STAGE + (size_t)(4 + ZMAX) * VS) +
                                  2 * STAGES * sizeof(unsigned long long);
 };
 
@@ -369,10 +374,11 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
   extern __shared__ __align__(16) double smem[];
   double* ring = smem;
   double* t = ring + STAGES * STAGE;
-  double* u = t + NT * DC;
-  double* corr = u + NT * DC;
-  double* zc = corr + 2 * NT * DC;
-  unsigned long long* full_bar = reinterpret_cast<unsigned long long*>(zc + T::ZMAX * NT * DC);
+  constexpr int VS = T::VS;
+  double* u = t + VS;
+  double* corr = u + VS;
+  double* zc = corr + 2 * VS;
+  unsigned long long* full_bar = reinterpret_cast<unsigned long long*>(zc + T::ZMAX * VS);
   unsigned long long* empty_bar = full_bar + STAGES;
   if (error_raised(a.err)) return;
   const int n = NT, d = a.d, mode = a.mode;
@@ -454,7 +460,7 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
   constexpr int TW = NT < 16 ? 1 : NT / 16;
   constexpr bool X4 = NT == 64 && DC == 4;  // transposed products on all consumer warps
   // shared-memory vectors (t, u, z cache, corrections): row-major [r][c], column-major at X4
-  auto vi = [](int r, int c) { return X4 ? c * NT + r : r * DC + c; };
+  auto vi = [](int r, int c) { return X4 ? c * kXLD + r : r * DC + c; };
   constexpr int CW = NT < 16 ? NT : 16, PR = CW / 2;
   const int rr = tid >> 2;
   const bool rlead = (tid & 3) == 0;
@@ -476,6 +482,16 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
       step_kind(mode, J, idx, kind, j);
       const long long row = start + j;
       BTD_SPH(0);
+      // X4 backward steps without the z cache: this lane's z_j entry (the one it combines in the
+      // transposed product, lane-fixed) is read from the solution buffer before the slot wait, so
+      // its L2 latency is not on the step's critical path
+      double zpre = 0.0;
+      if constexpr (X4) {
+        if (kind == kStepB && j >= T::ZMAX) {
+          const int oc = 8 * warp + 2 * (lane & 3) + (lane >> 4), orc = (lane >> 2) & 3;
+          if (orc < dc) zpre = a.x[row * ps + (size_t)oc * d + c0 + orc];
+        }
+      }
       mbar_wait(&full_bar[slot], phase);
       BTD_SPH(1);
       const double* sf = ring + slot * STAGE;
@@ -487,7 +503,7 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
         if (c < dc) v = vec_bulk ? sv[r * d + c] : a.rhs[row * ps + (size_t)r * d + c0 + c];
         if (mode == kSolveUp) {
           if (j == 0) v -= corr[vi(r, c)];
-          if (j == J - 1) v -= corr[NT * DC + vi(r, c)];
+          if (j == J - 1) v -= corr[VS + vi(r, c)];
         }
         return v;
       };
@@ -511,7 +527,7 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
         double sm[DC];
         mv_packed_rows<NT, DC>(sp, t, sm);
         if (rlead) {
-          double* zdst = j < T::ZMAX ? zc + j * NT * DC : nullptr;
+          double* zdst = j < T::ZMAX ? zc + j * VS : nullptr;
 #pragma unroll
           for (int c = 0; c < DC; ++c) {
             u[vi(rr, c)] = sm[c];
@@ -523,7 +539,7 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
         csync<NT>();
         BTD_SPH(5);
       } else if (kind == kStepB) {
-        const double* zsrc = j < T::ZMAX ? zc + j * NT * DC : nullptr;
+        const double* zsrc = j < T::ZMAX ? zc + j * VS : nullptr;
         auto zval = [&](int r, int c) -> double {
           return zsrc ? zsrc[vi(r, c)] : (c < dc ? a.x[row * ps + (size_t)r * d + c0 + c] : 0.0);
         };
@@ -532,7 +548,7 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
           if constexpr (X4) {
             int oc, orc;
             const double ov = mtv64x4<false>(sf, u, oc, orc);
-            t[vi(oc, orc)] = zval(oc, orc) - ov;
+            t[vi(oc, orc)] = (zsrc ? zsrc[vi(oc, orc)] : zpre) - ov;
           } else if (warp < TW) {
             double v[2][DC];
             mtv<NT, DC, false>(sf, u, v);
@@ -549,7 +565,9 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
           BTD_SPH(7);
           src = t;
         } else if (!zsrc) {
-          for (int e = tid; e < NT * DC; e += NTH) t[vi(e / DC, e % DC)] = zval(e / DC, e % DC);
+          if constexpr (X4) t[vi(8 * warp + 2 * (lane & 3) + (lane >> 4), (lane >> 2) & 3)] = zpre;
+          else
+            for (int e = tid; e < NT * DC; e += NTH) t[vi(e / DC, e % DC)] = zval(e / DC, e % DC);
           csync<NT>();
           src = t;
         }
@@ -623,15 +641,15 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
         } else if constexpr (X4) {
           int oc, orc;
           const double ov = mtv64x4<false>(sf, t, oc, orc);
-          corr[NT * DC + vi(oc, orc)] = ov;
+          corr[VS + vi(oc, orc)] = ov;
         } else if (warp < TW) {
           double v[2][DC];
           mtv<NT, DC, false>(sf, t, v);
           if (tlead) {
 #pragma unroll
             for (int c = 0; c < DC; ++c) {
-              corr[NT * DC + vi(tc, c)] = v[0][c];
-              corr[NT * DC + vi(tc + 1, c)] = v[1][c];
+              corr[VS + vi(tc, c)] = v[0][c];
+              corr[VS + vi(tc + 1, c)] = v[1][c];
             }
           }
         }
