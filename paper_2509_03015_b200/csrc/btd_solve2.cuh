@@ -194,6 +194,51 @@ __device__ __forceinline__ void mtv(const double* __restrict__ M, const double* 
 // product's one-value-per-lane stores (8 columns x 4 rhs columns per warp) fall in 2 wavefronts.
 constexpr int kXLD = 72;
 
+// Row form at NT == 64, DC == 4: warp w owns rows 8w..8w+7, lane half h = lane / 16 the rows
+// 8w + 4h + i (i < 4), and lane q = lane % 16 the column pairs (2q, 2q+1) and (32+2q, 33+2q), so
+// each half-warp reads one contiguous 256-byte run per load and holds 16 partials (4 rows x 4 rhs
+// columns), reduced over the 16 lanes of the half by a transposing butterfly (8+4+2+1 shuffles,
+// against 36 for mv64 at d = 4).  Lane l ends with row 8w + l / 4 (= tid / 4), rhs column l % 4.
+template <bool PACKED>
+__device__ __forceinline__ double mv64x4(const double* __restrict__ M, const double* __restrict__ x) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int ca = 2 * (lane & 15), cb = 32 + ca, r0 = 8 * w + 4 * (lane >> 4);
+  double2 xa[4], xb[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    xa[c] = *reinterpret_cast<const double2*>(x + c * kXLD + ca);
+    xb[c] = *reinterpret_cast<const double2*>(x + c * kXLD + cb);
+  }
+  double a[16];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = r0 + i;
+    double2 ea = make_double2(0.0, 0.0), eb = make_double2(0.0, 0.0);
+    if (!PACKED) {
+      ea = *reinterpret_cast<const double2*>(M + r * 64 + ca);
+      eb = *reinterpret_cast<const double2*>(M + r * 64 + cb);
+    } else {
+      if (ca <= r) ea = *reinterpret_cast<const double2*>(M + packed_row_offset(r) + ca);
+      if (cb <= r) eb = *reinterpret_cast<const double2*>(M + packed_row_offset(r) + cb);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      a[i * 4 + c] = fma(eb.y, xb[c].y, fma(eb.x, xb[c].x, fma(ea.y, xa[c].y, ea.x * xa[c].x)));
+  }
+#pragma unroll
+  for (int o = 8, h = 8; o >= 1; o >>= 1, h >>= 1) {
+    const bool hi = lane & o;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k < h) {
+        const double snd = hi ? a[k] : a[k + h], kp = hi ? a[k + h] : a[k];
+        a[k] = kp + __shfl_xor_sync(0xffffffffu, snd, o);
+      }
+    }
+  }
+  return a[0];
+}
+
 // Transposed form at NT == 64, DC == 4 on all 8 consumer warps (the 4-warp mtv leaves half the
 // consumers idle on the backward sweep, the longer half of the step at d = 4): warp w owns the 8
 // columns 8w..8w+7, lane = column pair p (lane % 4) + 4 part, part sweeping rows part, part + 8, ...
@@ -512,10 +557,15 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
         // t = b_j - L_{j,j-1} z_{j-1}
         if (j > 0) {
           double sm[DC];
-          mv_full_rows<NT, DC>(sf, u, sm);
-          if (rlead) {
+          if constexpr (X4) {
+            const double sv4 = mv64x4<false>(sf, u);
+            t[vi(rr, lane & 3)] = bval(rr, lane & 3) - sv4;
+          } else {
+            mv_full_rows<NT, DC>(sf, u, sm);
+            if (rlead) {
 #pragma unroll
-            for (int c = 0; c < DC; ++c) t[vi(rr, c)] = bval(rr, c) - sm[c];
+              for (int c = 0; c < DC; ++c) t[vi(rr, c)] = bval(rr, c) - sm[c];
+            }
           }
         } else {
           for (int e = tid; e < NT * DC; e += NTH) t[vi(e / DC, e % DC)] = bval(e / DC, e % DC);
@@ -525,6 +575,13 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
         BTD_SPH(3);
         // z_j = Linv_j t
         double sm[DC];
+        if constexpr (X4) {
+          const double sv4 = mv64x4<true>(sp, t);
+          const int c = lane & 3;
+          u[vi(rr, c)] = sv4;
+          if (j < T::ZMAX) zc[j * VS + vi(rr, c)] = sv4;
+          else if (c < dc) a.x[row * ps + (size_t)rr * d + c0 + c] = sv4;
+        } else {
         mv_packed_rows<NT, DC>(sp, t, sm);
         if (rlead) {
           double* zdst = j < T::ZMAX ? zc + j * VS : nullptr;
@@ -534,6 +591,7 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
             if (zdst) zdst[vi(rr, c)] = sm[c];
             else if (c < dc) a.x[row * ps + (size_t)rr * d + c0 + c] = sm[c];
           }
+        }
         }
         BTD_SPH(4);
         csync<NT>();
@@ -597,11 +655,16 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
         double* dst = (kind == kStepCR ? a.fr : a.fl) + (size_t)k * ps;
         if (kind == kStepCR) {
           double sm[DC];
-          mv_full_rows<NT, DC>(sf, u, sm);
-          if (rlead) {
+          if constexpr (X4) {
+            const double sv4 = mv64x4<false>(sf, u);
+            if ((lane & 3) < dc) dst[(size_t)rr * d + c0 + (lane & 3)] = sv4;
+          } else {
+            mv_full_rows<NT, DC>(sf, u, sm);
+            if (rlead) {
 #pragma unroll
-            for (int c = 0; c < DC; ++c)
-              if (c < dc) dst[(size_t)rr * d + c0 + c] = sm[c];
+              for (int c = 0; c < DC; ++c)
+                if (c < dc) dst[(size_t)rr * d + c0 + c] = sm[c];
+            }
           }
         } else if constexpr (X4) {
           int oc, orc;
@@ -633,10 +696,14 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
         csync<NT>();
         if (kind == kStepCL) {
           double sm[DC];
-          mv_full_rows<NT, DC>(sf, t, sm);
-          if (rlead) {
+          if constexpr (X4) {
+            corr[vi(rr, lane & 3)] = mv64x4<false>(sf, t);
+          } else {
+            mv_full_rows<NT, DC>(sf, t, sm);
+            if (rlead) {
 #pragma unroll
-            for (int c = 0; c < DC; ++c) corr[vi(rr, c)] = sm[c];
+              for (int c = 0; c < DC; ++c) corr[vi(rr, c)] = sm[c];
+            }
           }
         } else if constexpr (X4) {
           int oc, orc;
