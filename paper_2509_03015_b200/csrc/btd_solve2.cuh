@@ -288,6 +288,34 @@ __device__ __forceinline__ double mtv64x4(const double* __restrict__ M, const do
   return v;
 }
 
+// Transposed form at NT == 64, DC == 1 on all 8 consumer warps (mtv64x4's mapping): warp w owns
+// columns 8w..8w+7, lane = column pair (lane % 4) + 4 part, part sweeping rows part + 8i; the two
+// column partials are split over lane bit 4 and reduced over the parts (3 shuffles).  The total of
+// column 8w + 2 (lane % 4) + lane / 16 ends on the 4 lanes with equal lane % 4 and lane / 16.
+template <bool PACKED>
+__device__ __forceinline__ double mtv64x1(const double* __restrict__ M, const double* __restrict__ x, int& col) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int part = lane >> 2, c2 = 8 * w + 2 * (lane & 3);
+  double a[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int m = part + 8 * i;
+    double2 e = make_double2(0.0, 0.0);
+    if (!PACKED) e = *reinterpret_cast<const double2*>(M + m * 64 + c2);
+    else if (c2 <= m) e = *reinterpret_cast<const double2*>(M + packed_row_offset(m) + c2);
+    const double xv = x[m];
+    a[i & 1][0] = fma(e.x, xv, a[i & 1][0]);
+    a[i & 1][1] = fma(e.y, xv, a[i & 1][1]);
+  }
+  const double a0 = a[0][0] + a[1][0], a1 = a[0][1] + a[1][1];
+  const bool hi = lane & 16;
+  double v = (hi ? a1 : a0) + __shfl_xor_sync(0xffffffffu, hi ? a0 : a1, 16);
+  v += __shfl_xor_sync(0xffffffffu, v, 8);
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  col = c2 + (lane >> 4);
+  return v;
+}
+
 // Row form at NT == 64 without the rotated reads: warp w owns rows 8w..8w+7 and lane l the column
 // pair (2l, 2l+1), so each row read is one contiguous conflict-free 512-byte run and x[2l..2l+1]
 // is loaded once into registers; the 8 row partials are reduced across the warp by a
@@ -504,6 +532,8 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
   // column inside one warp (xor-shuffle reduction, no shared-memory partials).
   constexpr int TW = NT < 16 ? 1 : NT / 16;
   constexpr bool X4 = NT == 64 && DC == 4;  // transposed products on all consumer warps
+  constexpr bool X1 = NT == 64 && DC == 1;  // backward-sweep transposed products on all warps
+  const bool x1lead = ((lane >> 2) & 3) == 0;
   // shared-memory vectors (t, u, z cache, corrections): row-major [r][c], column-major at X4
   auto vi = [](int r, int c) { return X4 ? c * kXLD + r : r * DC + c; };
   constexpr int CW = NT < 16 ? NT : 16, PR = CW / 2;
@@ -607,6 +637,10 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
             int oc, orc;
             const double ov = mtv64x4<false>(sf, u, oc, orc);
             t[vi(oc, orc)] = (zsrc ? zsrc[vi(oc, orc)] : zpre) - ov;
+          } else if constexpr (X1) {
+            int oc;
+            const double ov = mtv64x1<false>(sf, u, oc);
+            if (x1lead) t[oc] = zval(oc, 0) - ov;
           } else if (warp < TW) {
             double v[2][DC];
             mtv<NT, DC, false>(sf, u, v);
@@ -635,6 +669,13 @@ __global__ void __launch_bounds__(TmaShape<NT, DC, WIDE>::NTHREADS, TmaShape<NT,
           const double ov = mtv64x4<true>(sp, src, oc, orc);
           u[vi(oc, orc)] = ov;
           if (mode != kSolveDown && orc < dc) a.x[row * ps + (size_t)oc * d + c0 + orc] = ov;
+        } else if constexpr (X1) {
+          int oc;
+          const double ov = mtv64x1<true>(sp, src, oc);
+          if (x1lead) {
+            u[oc] = ov;
+            if (mode != kSolveDown) a.x[row * ps + (size_t)oc * d + c0] = ov;
+          }
         } else if (warp < TW) {
           double v[2][DC];
           mtv<NT, DC, true>(sp, src, v);
