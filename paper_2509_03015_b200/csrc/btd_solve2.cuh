@@ -239,6 +239,45 @@ __device__ __forceinline__ double mv64x4(const double* __restrict__ M, const dou
   return a[0];
 }
 
+// Row form at NT == 64, DC == 1 with mv64x4's half-warp row groups: 4 partials per lane, a
+// transposing butterfly over lane bits 3, 2 then two plain levels (5 shuffles instead of mv64's 9);
+// the total of row 8w + l / 4 (= tid / 4) ends on the 4 lanes of that row's quad (mv64's mapping).
+template <bool PACKED>
+__device__ __forceinline__ double mv64x1(const double* __restrict__ M, const double* __restrict__ x) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int ca = 2 * (lane & 15), cb = 32 + ca, r0 = 8 * w + 4 * (lane >> 4);
+  const double2 xa = *reinterpret_cast<const double2*>(x + ca);
+  const double2 xb = *reinterpret_cast<const double2*>(x + cb);
+  double a[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = r0 + i;
+    double2 ea = make_double2(0.0, 0.0), eb = make_double2(0.0, 0.0);
+    if (!PACKED) {
+      ea = *reinterpret_cast<const double2*>(M + r * 64 + ca);
+      eb = *reinterpret_cast<const double2*>(M + r * 64 + cb);
+    } else {
+      if (ca <= r) ea = *reinterpret_cast<const double2*>(M + packed_row_offset(r) + ca);
+      if (cb <= r) eb = *reinterpret_cast<const double2*>(M + packed_row_offset(r) + cb);
+    }
+    a[i] = fma(eb.y, xb.y, fma(eb.x, xb.x, fma(ea.y, xa.y, ea.x * xa.x)));
+  }
+  {
+    const bool hi = lane & 8;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double snd = hi ? a[k] : a[k + 2], kp = hi ? a[k + 2] : a[k];
+      a[k] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+    }
+  }
+  const bool hi = lane & 4;
+  const double snd = hi ? a[0] : a[1], kp = hi ? a[1] : a[0];
+  double v = kp + __shfl_xor_sync(0xffffffffu, snd, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v;
+}
+
 // Transposed form at NT == 64, DC == 4 on all 8 consumer warps (the 4-warp mtv leaves half the
 // consumers idle on the backward sweep, the longer half of the step at d = 4): warp w owns the 8
 // columns 8w..8w+7, lane = column pair p (lane % 4) + 4 part, part sweeping rows part, part + 8, ...
@@ -382,11 +421,13 @@ __device__ __forceinline__ void mv64(const double* __restrict__ M, const double*
 
 template <int NT, int DC>
 __device__ __forceinline__ void mv_full_rows(const double* M, const double* x, double (&s)[DC]) {
+  if constexpr (NT == 64 && DC == 1) { s[0] = mv64x1<false>(M, x); return; }
   if constexpr (NT == 64) { mv64<DC, false, DC == 4>(M, x, s); return; }
   mv_rows<NT, DC>(M, x, s);
 }
 template <int NT, int DC>
 __device__ __forceinline__ void mv_packed_rows(const double* M, const double* x, double (&s)[DC]) {
+  if constexpr (NT == 64 && DC == 1) { s[0] = mv64x1<true>(M, x); return; }
   if constexpr (NT == 64) { mv64<DC, true, DC == 4>(M, x, s); return; }
   mv_pack_rows<NT, DC>(M, x, s);
 }
